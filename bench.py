@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark: eager-verify neighbour sampling, BASELINE.json config 2.
+
+Workload (BASELINE.json configs[1]): 4-clique on RMAT scale 20, edge factor 16,
+(a,b,c,d) = (.57,.19,.19,.05), symmetrised, deduplicated, self-loops removed,
+degree-relabelled so the reference's id-order symmetry breaking equals
+degree-ordered orientation; synthetic (seeded generator), 1 GPU.
+
+A "step" = one pass of the hot path over one batch: B = 2^24 samples with
+global ids [step*B*N + rank*B, ...) drawn by the sampling kernel, folded into
+1000-sample convergence windows (window-moments kernel) — exactly the work of
+2^24/1000 windows of run_ns_online (ns_engine.cpp:106-140). For N>1 each step
+ends with an NCCL all-gather of the ranks' window moments (the convergence
+exchange); samples are sharded by id, so scaling is weak.
+
+Reported (one JSON line from rank 0):
+  value              verified samples/s, whole job, inputs resident in HBM
+  e2e                the same metric through the public C-ABI call with host
+                     buffers: graph upload from host CSR + run_fixed_budget +
+                     accumulator read-back, every step
+  time_to_converge   run_ns_online(eps=1%, delta=5%) wall time (1 GPU, graph resident)
+  roofline           B_min algorithmic bytes per sample x samples
+                     per launch / sampling-kernel event time vs measured HBM copy BW
+  cpu_baseline       the compiled reference (oracle/_ref) run_fixed_budget on all
+                     host cores over a bounded sample
+
+`--impl reference` times the reference's own CPU implementation instead.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "verified samples/s & time-to-converge (4-clique, 1%@95%); % HBM roofline"
+UNIT = "samples/s"
+CONFIG = {
+    "workload": "4clique NS on RMAT-20 ef16 (a,b,c,d)=(.57,.19,.19,.05), symmetrized/dedup/no-loops, "
+                "degree-relabelled; BASELINE.json configs[1]",
+    "graph": {"generator": "rmat", "scale": 20, "edge_factor": 16, "seed": 1},
+    "pattern": "4clique",
+    "verify": "eager",
+    "samples_per_step_per_gpu": 1 << 24,
+    "window": 1000,
+    "rng": "CounterRng(seed=1, 0, sample_id) (reference stream, workers=1 semantics)",
+    "l2": "inputs larger than L2 (graph 0.4 GB resident: nbr + vtx + seed arcs), no flush",
+}
+B = 1 << 24
+WINDOW = 1000
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def make_graph(A):
+    g = A.rmat(20, 16, 0.57, 0.19, 0.19, seed=1)
+    return g.relabel_by_degree()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index):
+        self.rows = []
+        self.proc = None
+        self.index = index
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 7:
+                for nm, v in zip(names, r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rate(off, nbr, m, budget_hint, seed=1, target_s=10.0):
+    """The compiled reference's run_fixed_budget on all host cores, bounded."""
+    from oracle_bindings import RefLib
+
+    R = RefLib()
+    rg = R.from_csr(off, nbr, m)
+    cores = os.cpu_count() or 1
+    t = time.perf_counter()
+    R.fixed_budget(rg, "4clique", 1 << 14, seed, cores)
+    dt = time.perf_counter() - t
+    n = int(min(budget_hint, max(1 << 15, (1 << 14) * target_s / max(dt, 1e-6))))
+    t = time.perf_counter()
+    acc = R.fixed_budget(rg, "4clique", n, seed, cores)
+    dt = time.perf_counter() - t
+    return n / dt, cores, n, dt, acc
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import numpy as np  # noqa: F401
+
+    import paper_2405_03488_b200 as A
+    from oracle_bindings import RefLib
+
+    g = make_graph(A)
+    off, nbr = g.arrays()
+    m = g.edge_count
+    R = RefLib()
+    rg = R.from_csr(off, nbr, m)
+    cores = os.cpu_count() or 1
+    # bound each step to ~3 s of CPU work
+    t = time.perf_counter()
+    R.fixed_budget(rg, "4clique", 1 << 14, 1, cores)
+    dt = time.perf_counter() - t
+    per_step = int(max(1 << 15, min(1 << 22, (1 << 14) * 3.0 / max(dt, 1e-6))))
+    for w in range(args.warmup):
+        R.fixed_budget(rg, "4clique", per_step, 1000 + w, cores)
+    t = time.perf_counter()
+    for s in range(args.steps):
+        R.fixed_budget(rg, "4clique", per_step, 1 + s, cores)
+    el = time.perf_counter() - t
+    value = per_step * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * el / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64",
+        "data": "synthetic", "config": dict(CONFIG, samples_per_step=per_step),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{per_step} samples/step of the workload, run_fixed_budget(workers={cores})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    import paper_2405_03488_b200 as A
+
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    A.lib()
+    A.lib().agpm_set_device(torch.cuda.current_device())
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    t0 = time.perf_counter()
+    g = make_graph(A)
+    gen_s = time.perf_counter() - t0
+    off, nbr = g.arrays()
+    m = g.edge_count
+    dg = A.DeviceGraph(g, stream=sptr)
+    plan = A.compile_plan("4clique", "eager")
+    info = dg.info()
+
+    values = torch.empty(B, dtype=torch.float64, device=dev)
+    nwin = (B + WINDOW - 1) // WINDOW
+    wins = torch.empty((nwin, 4), dtype=torch.float64, device=dev)  # 32-B accumulator records
+    gathered = torch.empty((world * nwin, 4), dtype=torch.float64, device=dev) if world > 1 else None
+
+    def step(s):
+        first = (s * world + rank) * B
+        A.sample_dev(dg, plan, 1, first, B, values.data_ptr(), sptr)
+        A.window_moments_dev(values.data_ptr(), B, WINDOW, wins.data_ptr(), sptr)
+        if dist is not None:
+            dist.all_gather_into_tensor(gathered, wins)
+
+    # algorithmic bytes per sample (B_min sector model), counted on device, untimed
+    bmin_total = A.bmin_bytes(dg, plan, 1, 0, 1 << 22, sptr)
+    bmin_per_sample = bmin_total / float(1 << 22)
+
+    for w in range(max(args.warmup, 0)):
+        step(10_000 + w)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    # sampling-kernel share: events around each sample launch, same stream
+    k_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = A.kernel_launches()
+    with Clocks(torch.cuda.current_device()) as clk:
+        ev0.record(stream)
+        for s in range(args.steps):
+            first = (s * world + rank) * B
+            k_start[s].record(stream)
+            A.sample_dev(dg, plan, 1, first, B, values.data_ptr(), sptr)
+            k_end[s].record(stream)
+            A.window_moments_dev(values.data_ptr(), B, WINDOW, wins.data_ptr(), sptr)
+            if dist is not None:
+                dist.all_gather_into_tensor(gathered, wins)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = A.kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    kern_ms = sum(a.elapsed_time(b) for a, b in zip(k_start, k_end)) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = B * world * args.steps / (ms / 1000.0)
+
+    # ---- e2e through the public C-ABI with host buffers (graph upload + fixed budget + read-back)
+    e2e_steps = max(1, min(args.steps, 3))
+    h2d = int(off.nbytes + nbr.nbytes)
+    d2h = int(((B + 4095) // 4096) * 32)
+    A.run_fixed_budget(A.DeviceGraph(g), plan, 1 << 16, 1)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t = time.perf_counter()
+    for s in range(e2e_steps):
+        dgh = A.DeviceGraph(g)
+        acc = A.run_fixed_budget(dgh, plan, B, 1 + s * world + rank)
+        del dgh
+    e2e_s = time.perf_counter() - t
+    if dist is not None:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_value = B * world * e2e_steps / e2e_s
+
+    # ---- time to converge (1%@95%) on the resident graph, rank 0's device
+    ttc = None
+    if rank == 0:
+        A.run_ns_online(dg, plan, 0.01, 0.05, A.OnlinePolicy(), seed=1)
+        r = A.run_ns_online(dg, plan, 0.01, 0.05, A.OnlinePolicy(), seed=1)
+        ttc = {"seconds": r.seconds, "samples": r.report.n, "windows": r.windows,
+               "samples_launched": r.samples_launched, "estimate": r.report.mu,
+               "epsilon_hat": r.report.epsilon_hat, "hit_rate": r.report.hit_rate,
+               "converged": bool(r.report.converged)}
+
+    peak, peak_src = peaks()
+    achieved = bmin_per_sample * B / (kern_ms / 1000.0) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("workload") == CONFIG["workload"] and tr.get("samples_per_launch") == B:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            rate, cores, n, dt, _ = cpu_reference_rate(off, nbr, m, 1 << 22)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"{n} samples of the same workload (run_fixed_budget, workers={cores}) in {dt:.1f} s"}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic (seeded RMAT generator, no dataset)",
+            "config": dict(CONFIG, parallelism=f"samples sharded by id over {world} GPU(s)",
+                           graph_stats={"n": info["vertex_count"], "m": info["edge_count"],
+                                        "device_bytes": info["device_bytes"], "gen_s": round(gen_s, 2)}),
+            "time_to_converge": ttc,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "what": "DeviceGraph(host CSR) upload + run_fixed_budget(2^24) + accumulator read-back"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "bmin_bytes_per_sample": bmin_per_sample, "kernel_ms": kern_ms,
+                         "kernel_share_of_step": kern_ms / ms_per_step},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,215 @@
+/*
+ * agpm_b200.h — C-ABI boundary of the B200-native ScaleGPM sampling hot path.
+ *
+ * Everything here is plain C: fixed-size structs, raw pointers, sizes and an
+ * int status (AGPM_OK or an AGPM_E* code) with a thread-local message from
+ * agpm_last_error(). No torch or C++ types cross this line. The C++ drop-in
+ * API (include/agpm/ headers, namespace agpm) and the Python mirror
+ * (paper_2405_03488_b200/__init__.py) are thin wrappers over these calls.
+ *
+ * Each entry point names the reference interface it replaces
+ * (reference = /root/reference/proj, "agpm" C++20 library).
+ *
+ * Stream semantics: every call that takes `void* stream` accepts a
+ * cudaStream_t (NULL = the library's own per-device stream). Calls that return
+ * host results synchronise that stream before returning; *_dev calls only
+ * enqueue work.
+ */
+#ifndef AGPM_B200_H_
+#define AGPM_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AGPM_B200_ABI_VERSION 1
+
+/* status codes; the C++ wrapper rethrows them as the reference's exception types */
+#define AGPM_OK 0
+#define AGPM_E_INVALID 1   /* std::invalid_argument   (e.g. ns_engine.cpp:94-95,108-110) */
+#define AGPM_E_PATTERN 2   /* agpm::pattern_error      (pattern.hpp:49-51) */
+#define AGPM_E_IO 3        /* agpm::io_error           (csr_graph.hpp:15-17) */
+#define AGPM_E_PARSE 4     /* agpm::parse_error        (csr_graph.hpp:12-14) */
+#define AGPM_E_CUDA 5      /* device failure (no reference analogue) */
+#define AGPM_E_NODEVICE 6  /* no CUDA device: the product has no CPU fallback */
+#define AGPM_E_INTERNAL 7
+
+#define AGPM_MAX_K 9
+#define AGPM_MAX_PAIRS 36 /* C(9,2) */
+
+/* ---------------------------------------------------------------- plans ---
+ * Mirrors agpm::PlanStep / agpm::ExecutionPlan (plan.hpp:21-55). Position
+ * lists keep the reference's element order. */
+typedef struct agpm_plan_step {
+  int32_t pattern_vertex;
+  int32_t n_in, in_positions[AGPM_MAX_K];
+  int32_t n_out, out_positions[AGPM_MAX_K];
+  int32_t n_gt, greater_than[AGPM_MAX_K];
+  int32_t n_lt, less_than[AGPM_MAX_K];
+  int32_t tree_parent;
+  int32_t n_verify, verify_edges[AGPM_MAX_K][2];
+} agpm_plan_step;
+
+typedef struct agpm_plan {
+  char name[64];
+  int32_t k;                /* pattern.vertex_count */
+  int32_t induced;          /* 0 = Edge, 1 = Vertex (pattern.hpp:11) */
+  int32_t n_edges, edges[AGPM_MAX_PAIRS][2];
+  uint32_t adjacency[AGPM_MAX_K];
+  int32_t verify_mode;      /* 0 = Eager, 1 = Lazy (plan.hpp:14) */
+  int32_t order[AGPM_MAX_K], pos_of[AGPM_MAX_K];
+  int32_t seed_ordered, symmetry_enabled;
+  int32_t n_steps;
+  agpm_plan_step steps[AGPM_MAX_K - 2];
+  int32_t n_closure, closure_edges[AGPM_MAX_PAIRS][2];
+  int32_t n_constraints, constraints[AGPM_MAX_PAIRS][2];
+  int32_t n_terminal, terminal_constraints[AGPM_MAX_PAIRS][2];
+} agpm_plan;
+
+/* replaces parse_pattern_spec + compile_plan (pattern.cpp:130-165, plan.cpp:57-137).
+ * induced_override: NULL/"" keep default, "edge", "vertex". */
+int agpm_plan_compile(const char* spec, const char* induced_override, int verify_mode,
+                      int enable_symmetry, agpm_plan* out);
+/* replaces builtin_pattern_names (pattern.cpp:140-148); '\n'-separated */
+int agpm_builtin_pattern_names(char* buf, size_t cap);
+/* replaces Pattern::automorphisms().size() (pattern.cpp:43-57) */
+int agpm_pattern_automorphism_count(const char* spec, const char* induced_override,
+                                    uint64_t* out);
+/* replaces ExecutionPlan::scaling_rule_text (plan.cpp:139-148) */
+int agpm_plan_scaling_rule(const agpm_plan* plan, char* buf, size_t cap);
+/* replaces plan_verifies_each_edge_once (plan.cpp:150-163) */
+int agpm_plan_verifies_each_edge_once(const agpm_plan* plan, int* out);
+
+/* ---------------------------------------------------------------- stats ---
+ * Mirrors SampleAccumulator / ConvergenceReport (stats.hpp:16-43). */
+typedef struct agpm_accumulator {
+  uint64_t n, hits;
+  double sum, squared_sum;
+} agpm_accumulator;
+
+typedef struct agpm_report {
+  double mu, sigma, epsilon_hat;
+  uint64_t n;
+  int32_t converged;
+  double hit_rate;
+} agpm_report;
+
+double agpm_norm_cdf(double z);                                   /* stats.cpp:8 */
+int agpm_inv_norm_cdf(double q, double* out);                      /* stats.cpp:45-55 */
+int agpm_predicted_error(const agpm_accumulator* acc, double delta,
+                         agpm_report* out);                        /* stats.cpp:57-70 */
+
+/* ------------------------------------------------------ host CSR graphs ---
+ * Owning host CSR, mirrors agpm::CsrGraph (csr_graph.hpp:46-80): u64 offsets,
+ * u32 sorted neighbours, symmetric unless oriented. */
+typedef struct agpm_host_graph agpm_host_graph;
+
+/* CsrGraph::from_edges (csr_graph.cpp:46-72); edges = 2*n_edges u32 */
+int agpm_host_graph_from_edges(const uint32_t* edges, uint64_t n_edges, uint32_t min_vertex_count,
+                               agpm_host_graph** out);
+/* adopt/copy an existing CSR (CsrGraph ctor, csr_graph.cpp:32-38) */
+int agpm_host_graph_from_csr(uint32_t n, uint64_t edge_count, const uint64_t* offsets,
+                             const uint32_t* neighbors, int oriented, agpm_host_graph** out);
+int agpm_host_graph_load(const char* path, agpm_host_graph** out);        /* load_graph_auto :162-170 */
+int agpm_host_graph_write_binary(const agpm_host_graph* g, const char* path); /* :109-122 */
+int agpm_host_graph_info(const agpm_host_graph* g, uint32_t* n, uint64_t* edge_count,
+                         uint64_t* arcs, int* oriented, uint64_t* max_degree);
+int agpm_host_graph_arrays(const agpm_host_graph* g, const uint64_t** offsets,
+                           const uint32_t** neighbors);
+void agpm_host_graph_free(agpm_host_graph* g);
+
+/* Relabel so vertex id = rank of (degree, id): the reference's id-order
+ * symmetry constraints then coincide with degree orientation. */
+int agpm_host_graph_relabel_by_degree(const agpm_host_graph* g, agpm_host_graph** out);
+/* orient_by_degree (csr_graph.cpp:172-188) */
+int agpm_host_graph_orient_by_degree(const agpm_host_graph* g, agpm_host_graph** out);
+
+/* Deterministic generators (all built on CounterRng, rng.hpp:26-56).
+ * er_pairs: the reference test generator er_graph (test_graphs.hpp:37-43), O(n^2).
+ * er_fast: G(n, m_target) by uniform pair draws, O(m).
+ * rmat: scale/edge_factor/(a,b,c) quadrant recursion, undirected, dedup, no loops.
+ * planted: adds `count` k-cliques on uniformly drawn vertex k-sets. */
+int agpm_gen_er_pairs(uint32_t n, double p, uint64_t seed, agpm_host_graph** out);
+int agpm_gen_er_fast(uint32_t n, uint64_t target_edges, uint64_t seed, uint32_t planted_k,
+                     uint32_t planted_count, agpm_host_graph** out);
+int agpm_gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                  uint64_t seed, agpm_host_graph** out);
+
+/* ------------------------------------------------------ device graphs -----
+ * Device-resident mirror of a CsrView (csr_graph.hpp:23-41). Created from
+ * HOST arrays (copied over), or produced on device by sparsification. */
+typedef struct agpm_graph agpm_graph;
+
+/* end == NULL means a plain view (end[u] = begin[u+1]) */
+int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, const uint64_t* end,
+                      const uint32_t* neighbors, uint64_t neighbor_len, int oriented, void* stream,
+                      agpm_graph** out);
+int agpm_graph_upload_host(const agpm_host_graph* g, void* stream, agpm_graph** out);
+int agpm_graph_free(agpm_graph* g);
+int agpm_graph_info(const agpm_graph* g, uint32_t* n, uint64_t* edge_count, uint64_t* arcs,
+                    int* oriented, uint64_t* device_bytes);
+/* copy the view back to host (tests): begin[n], end[n], neighbors[neighbor_len] */
+int agpm_graph_download(const agpm_graph* g, uint64_t* begin, uint64_t* end, uint32_t* neighbors);
+
+/* ------------------------------------------------- neighbour sampling -----
+ * Global sample id i uses CounterRng(seed, 0, i) (rng.hpp:26-56), i.e. the
+ * reference's workers=1 streams (ns_engine.cpp:72): GPU results are
+ * sample-identical to the reference's single-worker run for every device and
+ * rank count. */
+typedef struct agpm_online_policy {
+  uint64_t n_min;              /* OnlinePolicy::n_min (ns_engine.hpp:40) */
+  uint64_t max_samples;        /* OnlinePolicy::max_samples */
+  uint64_t profiled_n_samples; /* OnlinePolicy::profiled_n_samples */
+} agpm_online_policy;
+
+typedef struct agpm_online_result {
+  agpm_report report;
+  agpm_accumulator accumulator;
+  uint64_t windows;
+  uint64_t work_units;   /* device: sample steps evaluated (not the CPU comparison count) */
+  uint64_t samples_launched; /* includes speculative samples past the stop window */
+  double seconds;        /* device wall time of the sampling loop */
+} agpm_online_result;
+
+/* draw_sample for ids [first_id, first_id+count) (ns_engine.cpp:92-104):
+ * values[i] = scaled value (0 on a miss), hits[i] in {0,1}, bindings
+ * (nullable) = count*k u32 matching-order bindings (0xffffffff past a miss). */
+int agpm_ns_draw(agpm_graph* g, const agpm_plan* plan, uint64_t seed, uint64_t first_id,
+                 uint64_t count, double* values, uint8_t* hits, uint32_t* bindings, void* stream);
+/* run_fixed_budget (ns_engine.cpp:142-153) */
+int agpm_ns_fixed_budget(agpm_graph* g, const agpm_plan* plan, uint64_t budget, uint64_t seed,
+                         agpm_accumulator* out, void* stream);
+/* run_ns_online (ns_engine.cpp:106-140), workers=1 window semantics */
+int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delta,
+                   const agpm_online_policy* policy, uint64_t seed, agpm_online_result* out,
+                   void* stream);
+
+/* Device-pointer building blocks (bench / multi-rank driver): enqueue only.
+ * d_values: count f64 device buffer. */
+int agpm_ns_sample_dev(agpm_graph* g, const agpm_plan* plan, uint64_t seed, uint64_t first_id,
+                       uint64_t count, double* d_values, void* stream);
+/* per-window moments (n, hits, sum, squared_sum) of d_values; windows of
+ * `window` samples aligned to d_values[0]; out = ceil(count/window) entries */
+int agpm_window_moments_dev(const double* d_values, uint64_t count, uint64_t window,
+                            agpm_accumulator* d_out, void* stream);
+/* Algorithmic bytes (SURVEY §8(d) B_min sector model) of ids [first, first+count),
+ * summed on device: a counting replay of the same sample paths. */
+int agpm_ns_bmin_bytes(agpm_graph* g, const agpm_plan* plan, uint64_t seed, uint64_t first_id,
+                       uint64_t count, uint64_t* total_bytes, void* stream);
+
+/* ------------------------------------------------------- misc / device -----*/
+const char* agpm_last_error(void);
+int agpm_device_count(int* n);
+int agpm_set_device(int device);
+int agpm_version(void);
+int agpm_sync(void* stream);
+/* kernels launched by this library since load (evidence for the bench) */
+uint64_t agpm_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AGPM_B200_H_ */

@@ -1,0 +1,383 @@
+"""B200-native ScaleGPM sampling hot path — Python mirror of the reference API.
+
+The product is libagpm_b200.so (host C++ + sm_100a kernels behind the C-ABI in
+include/agpm_b200.h). This module binds it with ctypes and mirrors the
+reference's agpm:: names and semantics (csr_graph.hpp, pattern.hpp, plan.hpp,
+stats.hpp, ns_engine.hpp) so callers and tests read like the reference's own:
+
+    g = CsrGraph.load("graph.bin")             # load_graph_auto
+    plan = compile_plan("4clique", "eager")   # parse_pattern_spec + compile_plan
+    dg = DeviceGraph(g)                        # device-resident CsrView
+    res = run_ns_online(dg, plan, 0.01, 0.05, OnlinePolicy(), seed=1)
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is visible, calls raise (ExtensionMissing / NoDeviceError).
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _abi
+from ._abi import Accumulator, OnlinePolicy, OnlineResult, Plan, Report
+
+__all__ = [
+    "AgpmError", "PatternError", "IoError", "ParseError", "CudaError", "NoDeviceError", "ExtensionMissing",
+    "lib", "compile_plan", "builtin_pattern_names", "automorphism_count", "scaling_rule_text",
+    "plan_verifies_each_edge_once", "norm_cdf", "inv_norm_cdf", "predicted_error", "CsrGraph",
+    "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
+    "hit_rate_report", "bmin_bytes", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libagpm_b200.so")
+
+
+class AgpmError(RuntimeError):
+    pass
+
+
+class PatternError(AgpmError):  # agpm::pattern_error (pattern.hpp:49-51)
+    pass
+
+
+class IoError(AgpmError):  # agpm::io_error (csr_graph.hpp:15-17)
+    pass
+
+
+class ParseError(AgpmError):  # agpm::parse_error (csr_graph.hpp:12-14)
+    pass
+
+
+class CudaError(AgpmError):
+    pass
+
+
+class NoDeviceError(AgpmError):
+    pass
+
+
+class ExtensionMissing(ImportError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load libagpm_b200.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ExtensionMissing(f"{LIB_PATH} is not built (run __graft_entry__.build()); "
+                                   "the sampling path has no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        _declare(L)
+        _lib = L
+    return _lib
+
+
+def _declare(L):
+    A = _abi
+    sig = {
+        "agpm_last_error": (C.c_char_p, []),
+        "agpm_version": (C.c_int, []),
+        "agpm_kernel_launches": (A.u64, []),
+        "agpm_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+        "agpm_set_device": (C.c_int, [C.c_int]),
+        "agpm_sync": (C.c_int, [A.P]),
+        "agpm_plan_compile": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_int, A.pPlan]),
+        "agpm_builtin_pattern_names": (C.c_int, [C.c_char_p, C.c_size_t]),
+        "agpm_pattern_automorphism_count": (C.c_int, [C.c_char_p, C.c_char_p, A.pu64]),
+        "agpm_plan_scaling_rule": (C.c_int, [A.pPlan, C.c_char_p, C.c_size_t]),
+        "agpm_plan_verifies_each_edge_once": (C.c_int, [A.pPlan, C.POINTER(C.c_int)]),
+        "agpm_norm_cdf": (C.c_double, [C.c_double]),
+        "agpm_inv_norm_cdf": (C.c_int, [C.c_double, A.pdbl]),
+        "agpm_predicted_error": (C.c_int, [A.pAcc, C.c_double, C.POINTER(Report)]),
+        "agpm_host_graph_from_edges": (C.c_int, [A.pu32, A.u64, A.u32, C.POINTER(A.P)]),
+        "agpm_host_graph_from_csr": (C.c_int, [A.u32, A.u64, A.pu64, A.pu32, C.c_int, C.POINTER(A.P)]),
+        "agpm_host_graph_load": (C.c_int, [C.c_char_p, C.POINTER(A.P)]),
+        "agpm_host_graph_write_binary": (C.c_int, [A.P, C.c_char_p]),
+        "agpm_host_graph_info": (C.c_int, [A.P, A.pu32, A.pu64, A.pu64, C.POINTER(C.c_int), A.pu64]),
+        "agpm_host_graph_arrays": (C.c_int, [A.P, C.POINTER(A.pu64), C.POINTER(A.pu32)]),
+        "agpm_host_graph_free": (None, [A.P]),
+        "agpm_host_graph_relabel_by_degree": (C.c_int, [A.P, C.POINTER(A.P)]),
+        "agpm_host_graph_orient_by_degree": (C.c_int, [A.P, C.POINTER(A.P)]),
+        "agpm_gen_er_pairs": (C.c_int, [A.u32, C.c_double, A.u64, C.POINTER(A.P)]),
+        "agpm_gen_er_fast": (C.c_int, [A.u32, A.u64, A.u64, A.u32, A.u32, C.POINTER(A.P)]),
+        "agpm_gen_rmat": (C.c_int, [A.u32, A.u32, C.c_double, C.c_double, C.c_double, A.u64, C.POINTER(A.P)]),
+        "agpm_graph_upload": (C.c_int, [A.u32, A.u64, A.pu64, A.pu64, A.pu32, A.u64, C.c_int, A.P, C.POINTER(A.P)]),
+        "agpm_graph_upload_host": (C.c_int, [A.P, A.P, C.POINTER(A.P)]),
+        "agpm_graph_free": (C.c_int, [A.P]),
+        "agpm_graph_info": (C.c_int, [A.P, A.pu32, A.pu64, A.pu64, C.POINTER(C.c_int), A.pu64]),
+        "agpm_graph_download": (C.c_int, [A.P, A.pu64, A.pu64, A.pu32]),
+        "agpm_ns_draw": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pdbl, A.pu8, A.pu32, A.P]),
+        "agpm_ns_fixed_budget": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.pAcc, A.P]),
+        "agpm_ns_online": (C.c_int, [A.P, A.pPlan, C.c_double, C.c_double, C.POINTER(OnlinePolicy), A.u64,
+                                     C.POINTER(OnlineResult), A.P]),
+        "agpm_ns_sample_dev": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.P, A.P]),
+        "agpm_window_moments_dev": (C.c_int, [A.P, A.u64, A.u64, A.P, A.P]),
+        "agpm_ns_bmin_bytes": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pu64, A.P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+
+
+def _check(status):
+    if status == _abi.OK:
+        return
+    msg = lib().agpm_last_error().decode(errors="replace")
+    exc = {
+        _abi.E_INVALID: ValueError,  # std::invalid_argument
+        _abi.E_PATTERN: PatternError,
+        _abi.E_IO: IoError,
+        _abi.E_PARSE: ParseError,
+        _abi.E_CUDA: CudaError,
+        _abi.E_NODEVICE: NoDeviceError,
+    }.get(status, AgpmError)
+    raise exc(msg)
+
+
+def _b(s):
+    return s.encode() if isinstance(s, str) else (s or b"")
+
+
+def _ptr(a, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+# ------------------------------------------------------------------ patterns / plans
+_MODES = {"eager": 0, "lazy": 1, 0: 0, 1: 1}
+
+
+def compile_plan(spec, mode="eager", enable_symmetry=True, induced=""):
+    """parse_pattern_spec(spec, induced) + compile_plan(p, mode, enable_symmetry)
+    (pattern.cpp:130-165, plan.cpp:57-137)."""
+    plan = Plan()
+    _check(lib().agpm_plan_compile(_b(spec), _b(induced), _MODES[mode], int(bool(enable_symmetry)),
+                                   C.byref(plan)))
+    return plan
+
+
+def builtin_pattern_names():
+    buf = C.create_string_buffer(4096)
+    _check(lib().agpm_builtin_pattern_names(buf, 4096))
+    return buf.value.decode().split()
+
+
+def automorphism_count(spec, induced=""):
+    out = C.c_uint64()
+    _check(lib().agpm_pattern_automorphism_count(_b(spec), _b(induced), C.byref(out)))
+    return out.value
+
+
+def scaling_rule_text(plan):
+    buf = C.create_string_buffer(512)
+    _check(lib().agpm_plan_scaling_rule(C.byref(plan), buf, 512))
+    return buf.value.decode()
+
+
+def plan_verifies_each_edge_once(plan):
+    out = C.c_int()
+    _check(lib().agpm_plan_verifies_each_edge_once(C.byref(plan), C.byref(out)))
+    return bool(out.value)
+
+
+# ------------------------------------------------------------------ stats
+def norm_cdf(z):
+    return lib().agpm_norm_cdf(z)
+
+
+def inv_norm_cdf(q):
+    out = C.c_double()
+    _check(lib().agpm_inv_norm_cdf(q, C.byref(out)))
+    return out.value
+
+
+def predicted_error(acc, delta):
+    rep = Report()
+    _check(lib().agpm_predicted_error(C.byref(acc), delta, C.byref(rep)))
+    return rep
+
+
+# ------------------------------------------------------------------ host graphs
+class CsrGraph:
+    """Owning host CSR (agpm::CsrGraph, csr_graph.hpp:46-80)."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value and _lib is not None:
+            _lib.agpm_host_graph_free(h)
+            self._h = None
+
+    @staticmethod
+    def _make(fn, *args):
+        h = C.c_void_p()
+        _check(fn(*args, C.byref(h)))
+        return CsrGraph(h)
+
+    @classmethod
+    def from_edges(cls, edges, min_vertex_count=0):
+        e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
+        return cls._make(lib().agpm_host_graph_from_edges, _ptr(e, C.c_uint32), e.shape[0], min_vertex_count)
+
+    @classmethod
+    def from_csr(cls, offsets, neighbors, edge_count, oriented=False):
+        o = np.ascontiguousarray(offsets, dtype=np.uint64)
+        nb = np.ascontiguousarray(neighbors, dtype=np.uint32)
+        return cls._make(lib().agpm_host_graph_from_csr, len(o) - 1, edge_count, _ptr(o, C.c_uint64),
+                         _ptr(nb, C.c_uint32), int(oriented))
+
+    @classmethod
+    def load(cls, path):
+        return cls._make(lib().agpm_host_graph_load, _b(path))
+
+    def write_binary(self, path):
+        _check(lib().agpm_host_graph_write_binary(self._h, _b(path)))
+
+    def _info(self):
+        n, m, arcs, o, md = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_int(), C.c_uint64()
+        _check(lib().agpm_host_graph_info(self._h, C.byref(n), C.byref(m), C.byref(arcs), C.byref(o), C.byref(md)))
+        return n.value, m.value, arcs.value, bool(o.value), md.value
+
+    @property
+    def vertex_count(self):
+        return self._info()[0]
+
+    @property
+    def edge_count(self):
+        return self._info()[1]
+
+    @property
+    def arc_count(self):
+        return self._info()[2]
+
+    @property
+    def oriented(self):
+        return self._info()[3]
+
+    def max_degree(self):
+        return self._info()[4]
+
+    def arrays(self):
+        """(offsets u64[n+1], neighbors u32[arcs]) as numpy copies."""
+        n, _, arcs, _, _ = self._info()
+        po, pn = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint32)()
+        _check(lib().agpm_host_graph_arrays(self._h, C.byref(po), C.byref(pn)))
+        off = np.ctypeslib.as_array(po, shape=(n + 1,)).copy()
+        nbr = np.ctypeslib.as_array(pn, shape=(arcs,)).copy() if arcs else np.zeros(0, np.uint32)
+        return off, nbr
+
+    def relabel_by_degree(self):
+        return CsrGraph._make(lib().agpm_host_graph_relabel_by_degree, self._h)
+
+    def orient_by_degree(self):
+        return CsrGraph._make(lib().agpm_host_graph_orient_by_degree, self._h)
+
+
+def er_graph(n, p, seed):
+    """The reference's er_graph (test_graphs.hpp:37-43), multi-threaded."""
+    return CsrGraph._make(lib().agpm_gen_er_pairs, n, p, seed)
+
+
+def er_fast(n, target_edges, seed, planted_k=0, planted_count=0):
+    return CsrGraph._make(lib().agpm_gen_er_fast, n, target_edges, seed, planted_k, planted_count)
+
+
+def rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1):
+    return CsrGraph._make(lib().agpm_gen_rmat, scale, edge_factor, a, b, c, seed)
+
+
+# ------------------------------------------------------------------ device graphs
+class DeviceGraph:
+    """Device-resident CsrView mirror (agpm_graph)."""
+
+    def __init__(self, graph=None, *, begin=None, end=None, neighbors=None, vertex_count=None, edge_count=None,
+                 oriented=False, stream=None):
+        h = C.c_void_p()
+        if graph is not None:
+            _check(lib().agpm_graph_upload_host(graph._h, stream, C.byref(h)))
+        else:
+            b = np.ascontiguousarray(begin, dtype=np.uint64)
+            e = None if end is None else np.ascontiguousarray(end, dtype=np.uint64)
+            nb = np.ascontiguousarray(neighbors, dtype=np.uint32)
+            n = vertex_count if vertex_count is not None else (len(b) - 1 if e is None else len(b))
+            _check(lib().agpm_graph_upload(n, edge_count, _ptr(b, C.c_uint64),
+                                           None if e is None else _ptr(e, C.c_uint64), _ptr(nb, C.c_uint32),
+                                           len(nb), int(oriented), stream, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value and _lib is not None:
+            _lib.agpm_graph_free(h)
+            self._h = None
+
+    def info(self):
+        n, m, arcs, o, by = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_int(), C.c_uint64()
+        _check(lib().agpm_graph_info(self._h, C.byref(n), C.byref(m), C.byref(arcs), C.byref(o), C.byref(by)))
+        return {"vertex_count": n.value, "edge_count": m.value, "arcs": arcs.value, "oriented": bool(o.value),
+                "device_bytes": by.value}
+
+
+def draw_samples(dg, plan, seed, first_id, count, with_bindings=True, stream=None):
+    """draw_sample for ids [first_id, first_id+count) with CounterRng(seed, 0, id)
+    (ns_engine.cpp:92-104). Returns (values f64, hits u8, bindings u32[count,k] or None)."""
+    values = np.zeros(count, np.float64)
+    hits = np.zeros(count, np.uint8)
+    binds = np.zeros((count, plan.k), np.uint32) if with_bindings else None
+    _check(lib().agpm_ns_draw(dg._h, C.byref(plan), seed, first_id, count, _ptr(values, C.c_double),
+                              _ptr(hits, C.c_uint8), None if binds is None else _ptr(binds, C.c_uint32), stream))
+    return values, hits, binds
+
+
+def run_fixed_budget(dg, plan, budget, seed, workers=1, stream=None):
+    """run_fixed_budget (ns_engine.cpp:142-153); device streams are the
+    reference's workers=1 streams whatever `workers` says."""
+    acc = Accumulator()
+    _check(lib().agpm_ns_fixed_budget(dg._h, C.byref(plan), budget, seed, C.byref(acc), stream))
+    return acc
+
+
+def hit_rate_report(dg, plan, sample_budget, seed, workers=1):
+    acc = run_fixed_budget(dg, plan, sample_budget, seed, workers)
+    return acc.hits / acc.n
+
+
+def run_ns_online(dg, plan, eps, delta, policy=None, seed=1, workers=1, stream=None):
+    """run_ns_online (ns_engine.cpp:106-140), workers=1 window semantics."""
+    res = OnlineResult()
+    pol = policy if policy is not None else OnlinePolicy()
+    _check(lib().agpm_ns_online(dg._h, C.byref(plan), eps, delta, C.byref(pol), seed, C.byref(res), stream))
+    return res
+
+
+def bmin_bytes(dg, plan, seed, first_id, count, stream=None):
+    out = C.c_uint64()
+    _check(lib().agpm_ns_bmin_bytes(dg._h, C.byref(plan), seed, first_id, count, C.byref(out), stream))
+    return out.value
+
+
+def sample_dev(dg, plan, seed, first_id, count, d_values_ptr, stream=None):
+    _check(lib().agpm_ns_sample_dev(dg._h, C.byref(plan), seed, first_id, count, C.c_void_p(d_values_ptr),
+                                    None if stream is None else C.c_void_p(stream)))
+
+
+def window_moments_dev(d_values_ptr, count, window, d_out_ptr, stream=None):
+    _check(lib().agpm_window_moments_dev(C.c_void_p(d_values_ptr), count, window, C.c_void_p(d_out_ptr),
+                                         None if stream is None else C.c_void_p(stream)))
+
+
+def kernel_launches():
+    return lib().agpm_kernel_launches()
+
+
+def device_count():
+    n = C.c_int()
+    _check(lib().agpm_device_count(C.byref(n)))
+    return n.value

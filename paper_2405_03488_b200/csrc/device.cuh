@@ -1,0 +1,73 @@
+// Device-resident graph mirror and per-device runtime context.
+//
+// HBM layout of one view:
+//   vtx[u]      16 B  {u64 begin, u32 degree, u32 up}: one 16-B load gives the
+//                     list bounds and `up` = #neighbours <= u, so the upper
+//                     suffix N+(u) = nbr[begin+up, begin+degree) is free.
+//   nbr[]        4 B  per arc, lists ascending (reference layout).
+//   seed_arcs[]  8 B  per view arc, (u << 32 | v) in arc-index order, so the
+//                     uniform seed arc of ns_engine.cpp:12-23 is ONE gather
+//                     instead of a log2(n) upper_bound over the prefix array.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "agpm_b200.h"
+#include "common.hpp"
+
+namespace agpm_b200 {
+
+struct __align__(16) VtxInfo {
+  unsigned long long begin;
+  unsigned int deg;
+  unsigned int up;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define AGPM_CUDA(x) ::agpm_b200::cuda_check((x), #x)
+
+struct DeviceCtx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  // grow-only scratch
+  void* scratch[8] = {nullptr};
+  size_t scratch_bytes[8] = {0};
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  void* get(int slot, size_t bytes);
+  void* get_pinned(size_t bytes);
+};
+
+DeviceCtx& ctx_for_current_device();
+cudaStream_t pick_stream(void* stream);
+void count_launch(uint64_t n = 1);
+
+}  // namespace agpm_b200
+
+// C-ABI opaque handle
+struct agpm_graph {
+  int device = 0;
+  uint32_t n = 0;
+  uint64_t edge_count = 0;
+  uint64_t arcs = 0;       // view arc total (seed space)
+  uint64_t nbr_len = 0;
+  uint64_t max_degree = 0;
+  bool oriented = false;
+  bool plain = true;       // end[u] == begin[u+1] and begin[0] == 0
+  agpm_b200::VtxInfo* vtx = nullptr;
+  uint32_t* nbr = nullptr;
+  unsigned long long* seed_arcs = nullptr;
+  uint64_t bytes = 0;
+};
+
+namespace agpm_b200 {
+// Build vtx / seed_arcs / arcs / max_degree for a view whose begin/end arrays
+// already sit on the device (d_end may be null for plain views). Takes
+// ownership of nothing; g->nbr must be set.
+void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsigned long long* d_end,
+                   cudaStream_t s);
+}  // namespace agpm_b200

@@ -1,0 +1,257 @@
+// Device graph mirror (CsrView on HBM), per-device context, misc C-ABI.
+#include <cub/cub.cuh>
+
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "device.cuh"
+
+namespace agpm_b200 {
+
+namespace {
+thread_local std::string t_err;
+std::atomic<uint64_t> g_launches{0};
+std::mutex g_ctx_mu;
+DeviceCtx* g_ctx[64] = {nullptr};
+}  // namespace
+
+void set_last_error(const std::string& msg) { t_err = msg; }
+void count_launch(uint64_t n) { g_launches += n; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+      throw nodevice_error(std::string("no usable CUDA device (the B200 path has no CPU fallback): ") +
+                           cudaGetErrorString(e));
+    throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+void* DeviceCtx::get(int slot, size_t bytes) {
+  if (scratch_bytes[slot] < bytes) {
+    if (scratch[slot]) AGPM_CUDA(cudaFree(scratch[slot]));
+    size_t grow = bytes + bytes / 4;
+    AGPM_CUDA(cudaMalloc(&scratch[slot], grow));
+    scratch_bytes[slot] = grow;
+  }
+  return scratch[slot];
+}
+
+void* DeviceCtx::get_pinned(size_t bytes) {
+  if (pinned_bytes < bytes) {
+    if (pinned) AGPM_CUDA(cudaFreeHost(pinned));
+    AGPM_CUDA(cudaMallocHost(&pinned, bytes));
+    pinned_bytes = bytes;
+  }
+  return pinned;
+}
+
+DeviceCtx& ctx_for_current_device() {
+  int dev = 0;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw nodevice_error("no CUDA device visible: the B200 sampling path has no CPU fallback");
+  AGPM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (!g_ctx[dev]) {
+    auto* c = new DeviceCtx();
+    c->device = dev;
+    AGPM_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev));
+    AGPM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    g_ctx[dev] = c;
+  }
+  return *g_ctx[dev];
+}
+
+cudaStream_t pick_stream(void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : ctx_for_current_device().stream;
+}
+
+namespace {
+
+__global__ void vtx_kernel(const unsigned long long* __restrict__ begin,
+                           const unsigned long long* __restrict__ end, const uint32_t* __restrict__ nbr,
+                           uint32_t n, VtxInfo* __restrict__ vtx, unsigned long long* __restrict__ deg) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long b = begin[u];
+    unsigned long long e = end ? end[u] : begin[u + 1];
+    // up = #neighbours <= u  (lower_bound of u+1)
+    unsigned long long lo = b, hi = e;
+    while (lo < hi) {
+      unsigned long long mid = (lo + hi) >> 1;
+      if (nbr[mid] <= (uint32_t)u)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    VtxInfo v;
+    v.begin = b;
+    v.deg = (unsigned int)(e - b);
+    v.up = (unsigned int)(lo - b);
+    vtx[u] = v;
+    deg[u] = e - b;
+  }
+}
+
+// one warp per vertex: seed_arcs[prefix[u] + j] = u<<32 | nbr[begin[u] + j]
+__global__ void seed_arcs_kernel(const VtxInfo* __restrict__ vtx, const uint32_t* __restrict__ nbr,
+                                 const unsigned long long* __restrict__ prefix, uint32_t n,
+                                 unsigned long long* __restrict__ arcs) {
+  const int lane = threadIdx.x & 31;
+  uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t u = w; u < n; u += nw) {
+    VtxInfo v = vtx[u];
+    unsigned long long base = prefix[u];
+    unsigned long long hi = (unsigned long long)u << 32;
+    for (unsigned int j = lane; j < v.deg; j += 32) arcs[base + j] = hi | nbr[v.begin + j];
+  }
+}
+
+}  // namespace
+
+void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsigned long long* d_end,
+                   cudaStream_t s) {
+  const uint32_t n = g->n;
+  DeviceCtx& ctx = ctx_for_current_device();
+  AGPM_CUDA(cudaMalloc(&g->vtx, sizeof(VtxInfo) * (size_t)(n ? n : 1)));
+  unsigned long long* deg = nullptr;
+  unsigned long long* prefix = nullptr;
+  AGPM_CUDA(cudaMalloc(&deg, sizeof(unsigned long long) * ((size_t)n + 1)));
+  AGPM_CUDA(cudaMalloc(&prefix, sizeof(unsigned long long) * ((size_t)n + 1)));
+  int blocks = ctx.sm_count * 8;
+  if (n) {
+    vtx_kernel<<<blocks, 256, 0, s>>>(d_begin, d_end, g->nbr, n, g->vtx, deg);
+    count_launch();
+    AGPM_CUDA(cudaGetLastError());
+  }
+  AGPM_CUDA(cudaMemsetAsync(prefix, 0, sizeof(unsigned long long), s));
+  AGPM_CUDA(cudaMemsetAsync(deg + n, 0, sizeof(unsigned long long), s));
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, deg, prefix + 1, (int64_t)n, s);
+  size_t tmp_bytes2 = 0;
+  unsigned long long* red = nullptr;
+  AGPM_CUDA(cudaMalloc(&red, sizeof(unsigned long long)));
+  cub::DeviceReduce::Max(nullptr, tmp_bytes2, deg, red, (int64_t)n + 1, s);
+  void* tmp = ctx.get(7, std::max(tmp_bytes, tmp_bytes2) + 16);
+  if (n) {
+    AGPM_CUDA(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, deg, prefix + 1, (int64_t)n, s));
+  }
+  unsigned long long arcs = 0, maxd = 0;
+  AGPM_CUDA(cudaMemcpyAsync(&arcs, prefix + n, sizeof(arcs), cudaMemcpyDeviceToHost, s));
+  AGPM_CUDA(cub::DeviceReduce::Max(tmp, tmp_bytes2, deg, red, (int64_t)n + 1, s));
+  AGPM_CUDA(cudaMemcpyAsync(&maxd, red, sizeof(maxd), cudaMemcpyDeviceToHost, s));
+  AGPM_CUDA(cudaStreamSynchronize(s));
+  g->arcs = arcs;
+  g->max_degree = maxd;
+  AGPM_CUDA(cudaMalloc(&g->seed_arcs, sizeof(unsigned long long) * (size_t)(arcs ? arcs : 1)));
+  if (n && arcs) {
+    seed_arcs_kernel<<<blocks, 256, 0, s>>>(g->vtx, g->nbr, prefix, n, g->seed_arcs);
+    count_launch();
+    AGPM_CUDA(cudaGetLastError());
+  }
+  AGPM_CUDA(cudaStreamSynchronize(s));
+  AGPM_CUDA(cudaFree(deg));
+  AGPM_CUDA(cudaFree(prefix));
+  AGPM_CUDA(cudaFree(red));
+  g->bytes = sizeof(VtxInfo) * (uint64_t)n + 4ull * g->nbr_len + 8ull * arcs;
+}
+
+}  // namespace agpm_b200
+
+using namespace agpm_b200;
+
+extern "C" {
+
+const char* agpm_last_error(void) { return t_err.c_str(); }
+int agpm_version(void) { return AGPM_B200_ABI_VERSION; }
+uint64_t agpm_kernel_launches(void) { return g_launches.load(); }
+
+int agpm_device_count(int* n) {
+  return guarded([&] {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    *n = e == cudaSuccess ? c : 0;
+  });
+}
+
+int agpm_set_device(int device) {
+  return guarded([&] { AGPM_CUDA(cudaSetDevice(device)); });
+}
+
+int agpm_sync(void* stream) {
+  return guarded([&] { AGPM_CUDA(cudaStreamSynchronize(pick_stream(stream))); });
+}
+
+int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, const uint64_t* end,
+                      const uint32_t* neighbors, uint64_t neighbor_len, int oriented, void* stream,
+                      agpm_graph** out) {
+  return guarded([&] {
+    if (!begin || !out || (neighbor_len && !neighbors)) throw std::invalid_argument("null argument");
+    DeviceCtx& ctx = ctx_for_current_device();
+    cudaStream_t s = pick_stream(stream);
+    auto* g = new agpm_graph();
+    g->device = ctx.device;
+    g->n = n;
+    g->edge_count = edge_count;
+    g->oriented = oriented != 0;
+    g->nbr_len = neighbor_len;
+    g->plain = end == nullptr && begin[0] == 0;
+    unsigned long long *d_begin = nullptr, *d_end = nullptr;
+    size_t nb = end ? n : (size_t)n + 1;
+    AGPM_CUDA(cudaMalloc(&d_begin, sizeof(uint64_t) * (nb ? nb : 1)));
+    AGPM_CUDA(cudaMemcpyAsync(d_begin, begin, sizeof(uint64_t) * nb, cudaMemcpyHostToDevice, s));
+    if (end) {
+      AGPM_CUDA(cudaMalloc(&d_end, sizeof(uint64_t) * (n ? n : 1)));
+      AGPM_CUDA(cudaMemcpyAsync(d_end, end, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s));
+    }
+    AGPM_CUDA(cudaMalloc(&g->nbr, sizeof(uint32_t) * (neighbor_len ? neighbor_len : 1)));
+    if (neighbor_len)
+      AGPM_CUDA(cudaMemcpyAsync(g->nbr, neighbors, sizeof(uint32_t) * neighbor_len,
+                                cudaMemcpyHostToDevice, s));
+    finalize_view(g, d_begin, d_end, s);
+    AGPM_CUDA(cudaFree(d_begin));
+    if (d_end) AGPM_CUDA(cudaFree(d_end));
+    *out = g;
+  });
+}
+
+int agpm_graph_free(agpm_graph* g) {
+  return guarded([&] {
+    if (!g) return;
+    cudaFree(g->vtx);
+    cudaFree(g->nbr);
+    cudaFree(g->seed_arcs);
+    delete g;
+  });
+}
+
+int agpm_graph_info(const agpm_graph* g, uint32_t* n, uint64_t* edge_count, uint64_t* arcs,
+                    int* oriented, uint64_t* device_bytes) {
+  return guarded([&] {
+    if (n) *n = g->n;
+    if (edge_count) *edge_count = g->edge_count;
+    if (arcs) *arcs = g->arcs;
+    if (oriented) *oriented = g->oriented;
+    if (device_bytes) *device_bytes = g->bytes;
+  });
+}
+
+int agpm_graph_download(const agpm_graph* g, uint64_t* begin, uint64_t* end, uint32_t* neighbors) {
+  return guarded([&] {
+    std::vector<VtxInfo> v(g->n);
+    AGPM_CUDA(cudaMemcpy(v.data(), g->vtx, sizeof(VtxInfo) * g->n, cudaMemcpyDeviceToHost));
+    for (uint32_t u = 0; u < g->n; ++u) {
+      if (begin) begin[u] = v[u].begin;
+      if (end) end[u] = v[u].begin + v[u].deg;
+    }
+    if (neighbors && g->nbr_len)
+      AGPM_CUDA(cudaMemcpy(neighbors, g->nbr, 4 * g->nbr_len, cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+"""GPU parity for the eager-verify sampler.
+
+The CUDA path (through the C-ABI) against the C oracle restatement on the same
+seeded inputs: per-sample value, hit AND matching-order bindings must be
+bit-identical to the reference's draw_sample with stream CounterRng(seed, 0, id)
+(ns_engine.cpp:27-53); accumulators agree exactly in n/hits and to
+reduction-order rounding (relative 1e-12, the oracle's own streaming
+tolerance is 1e-9, acceptance_main.cpp:413) in sum / squared sum; the online
+run stops at the same n (ns_engine.cpp:106-140).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PATTERNS = ["triangle", "4clique", "5clique", "4cycle", "house", "5path", "dumbbell", "6clique",
+            "3motif-wedge", "4motif-path", "4motif-star", "4motif-diamond", "4motif-tailedtriangle",
+            "4motif-cycle", "3motif-triangle", "4motif-clique"]
+
+
+def _graphs(agpm):
+    # small ER graphs (reference generator) plain and degree-relabelled, a
+    # skewed RMAT graph whose hubs exercise the warp-cooperative path
+    out = {
+        "er200": agpm.er_graph(200, 0.08, 71),
+        "er200_rel": agpm.er_graph(200, 0.08, 71).relabel_by_degree(),
+        "er60_dense": agpm.er_graph(60, 0.5, 5).relabel_by_degree(),
+        "rmat12_rel": agpm.rmat(12, 16, seed=3).relabel_by_degree(),
+        "rmat12": agpm.rmat(12, 16, seed=3),
+    }
+    return out
+
+
+@pytest.fixture(scope="module")
+def graphs(agpm):
+    return _graphs(agpm)
+
+
+@pytest.mark.parametrize("name", ["er200", "er200_rel", "er60_dense", "rmat12_rel", "rmat12"])
+@pytest.mark.parametrize("pattern", PATTERNS)
+def test_draw_bit_exact(agpm, oracle, graphs, name, pattern):
+    g = graphs[name]
+    off, nbr = g.arrays()
+    m = g.edge_count
+    plan = agpm.compile_plan(pattern, "eager")
+    dg = agpm.DeviceGraph(g)
+    count = 6000 if plan.k <= 5 else 2500
+    first = 12345
+    v, h, b = agpm.draw_samples(dg, plan, 9, first, count)
+    ov, oh, ob = oracle.draw_records(off, nbr, m, plan, 9, first, count)
+    np.testing.assert_array_equal(h, oh)
+    np.testing.assert_array_equal(v, ov)  # bit-exact doubles
+    np.testing.assert_array_equal(b, ob)
+
+
+def test_config1_first_2pow16_bit_exact(agpm, oracle):
+    """Config 1 graph (er_graph(10^4, 20/9999, 1), degree-relabelled), triangle,
+    stream seed 1: the first 2^16 samples match record for record."""
+    g = agpm.er_graph(10000, 20 / 9999, 1).relabel_by_degree()
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan("triangle")
+    dg = agpm.DeviceGraph(g)
+    v, h, b = agpm.draw_samples(dg, plan, 1, 0, 1 << 16)
+    ov, oh, ob = oracle.draw_records(off, nbr, g.edge_count, plan, 1, 0, 1 << 16)
+    np.testing.assert_array_equal(v, ov)
+    np.testing.assert_array_equal(b, ob)
+
+
+def test_fixed_budget_matches_oracle(agpm, oracle):
+    g = agpm.rmat(11, 16, seed=5).relabel_by_degree()
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan("4clique")
+    dg = agpm.DeviceGraph(g)
+    acc = agpm.run_fixed_budget(dg, plan, 200000, 77)
+    o = oracle.fixed_budget(off, nbr, g.edge_count, plan, 200000, 77)
+    assert acc.n == o.n and acc.hits == o.hits
+    assert abs(acc.sum - o.sum) <= 1e-12 * abs(o.sum)
+    assert abs(acc.squared_sum - o.squared_sum) <= 1e-12 * abs(o.squared_sum)
+
+
+@pytest.mark.parametrize("pattern,eps", [("4clique", 0.05), ("triangle", 0.02), ("4cycle", 0.05)])
+def test_online_stops_where_oracle_stops(agpm, oracle, pattern, eps):
+    g = agpm.rmat(11, 16, seed=7).relabel_by_degree()
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan(pattern)
+    dg = agpm.DeviceGraph(g)
+    pol = agpm.OnlinePolicy()
+    r = agpm.run_ns_online(dg, plan, eps, 0.05, pol, seed=31)
+    o = oracle.ns_online(off, nbr, g.edge_count, plan, eps, 0.05, pol, 31)
+    assert r.report.converged == o.report.converged == 1
+    assert r.report.n == o.report.n and r.windows == o.windows
+    assert r.accumulator.hits == o.accumulator.hits
+    assert abs(r.report.mu - o.report.mu) <= 1e-12 * o.report.mu
+    assert abs(r.report.epsilon_hat - o.report.epsilon_hat) <= 1e-9 * o.report.epsilon_hat
+
+
+def test_online_cap_without_matches(agpm):
+    """Star graph has no triangle: the cap stops the run unconverged (test_ns_engine.cpp:148-158)."""
+    star = agpm.CsrGraph.from_edges([[0, i] for i in range(1, 5)], 5)
+    dg = agpm.DeviceGraph(star)
+    plan = agpm.compile_plan("triangle")
+    r = agpm.run_ns_online(dg, plan, 0.1, 0.01, agpm.OnlinePolicy(max_samples=5000), seed=3)
+    assert not r.report.converged
+    assert r.report.n == 5000 and r.accumulator.hits == 0
+    assert np.isinf(r.report.epsilon_hat)
+
+
+def test_t3_hits_with_scale_3(agpm):
+    """draw_sample on T3 hits with value 3 about 1/3 of the time (test_ns_engine.cpp:73-90)."""
+    tri = agpm.CsrGraph.from_edges([[0, 1], [1, 2], [0, 2]], 3)
+    dg = agpm.DeviceGraph(tri)
+    v, h, _ = agpm.draw_samples(dg, agpm.compile_plan("triangle"), 10, 0, 3000)
+    assert set(np.unique(v)) <= {0.0, 3.0}
+    assert abs(h.mean() - 1 / 3) < 0.05
+
+
+def test_errors_are_loud(agpm):
+    tri = agpm.CsrGraph.from_edges([[0, 1], [1, 2], [0, 2]], 3)
+    dg = agpm.DeviceGraph(tri)
+    with pytest.raises(ValueError):
+        agpm.run_ns_online(dg, agpm.compile_plan("triangle"), 1.5, 0.05)
+    empty = agpm.CsrGraph.from_edges(np.zeros((0, 2), np.uint32), 4)
+    with pytest.raises(ValueError):
+        agpm.draw_samples(agpm.DeviceGraph(empty), agpm.compile_plan("triangle"), 1, 0, 10)
+    oriented = agpm.DeviceGraph(tri.orient_by_degree())
+    with pytest.raises(ValueError):
+        agpm.draw_samples(oriented, agpm.compile_plan("triangle"), 1, 0, 10)
