@@ -198,8 +198,12 @@ def run_gpu(args):
     A.lib()
     A.lib().agpm_set_device(torch.cuda.current_device())
     dev = torch.device("cuda", torch.cuda.current_device())
-    stream = torch.cuda.current_stream()
+    # a dedicated stream: torch's default stream has handle 0, which the C-ABI
+    # reads as "the library's own stream"
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
+    assert sptr != 0
 
     t0 = time.perf_counter()
     g = make_graph(A)

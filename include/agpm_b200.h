@@ -11,7 +11,8 @@
  * (reference = /root/reference/proj, "agpm" C++20 library).
  *
  * Stream semantics: every call that takes `void* stream` accepts a
- * cudaStream_t (NULL = the library's own per-device stream). Calls that return
+ * cudaStream_t (NULL = the library's own non-blocking per-device stream; pass
+ * cudaStreamLegacy, (void*)1, for the legacy default stream). Calls that return
  * host results synchronise that stream before returning; *_dev calls only
  * enqueue work.
  */
@@ -186,6 +187,11 @@ int agpm_ns_fixed_budget(agpm_graph* g, const agpm_plan* plan, uint64_t budget, 
 int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delta,
                    const agpm_online_policy* policy, uint64_t seed, agpm_online_result* out,
                    void* stream);
+
+/* Sampler strategy: 0 = auto (default), 1 = one warp per sample
+ * (k-ary searches + coalesced chunk intersections), 2 = one lane per sample
+ * (tiny adjacency lists). All strategies draw identical samples. */
+int agpm_ns_set_strategy(int strategy);
 
 /* Device-pointer building blocks (bench / multi-rank driver): enqueue only.
  * d_values: count f64 device buffer. */

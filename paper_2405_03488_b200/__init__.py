@@ -26,7 +26,7 @@ __all__ = [
     "lib", "compile_plan", "builtin_pattern_names", "automorphism_count", "scaling_rule_text",
     "plan_verifies_each_edge_once", "norm_cdf", "inv_norm_cdf", "predicted_error", "CsrGraph",
     "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
-    "hit_rate_report", "bmin_bytes", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "hit_rate_report", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
 ]
 
@@ -118,6 +118,7 @@ def _declare(L):
         "agpm_ns_sample_dev": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.P, A.P]),
         "agpm_window_moments_dev": (C.c_int, [A.P, A.u64, A.u64, A.P, A.P]),
         "agpm_ns_bmin_bytes": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pu64, A.P]),
+        "agpm_ns_set_strategy": (C.c_int, [C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -371,6 +372,14 @@ def sample_dev(dg, plan, seed, first_id, count, d_values_ptr, stream=None):
 def window_moments_dev(d_values_ptr, count, window, d_out_ptr, stream=None):
     _check(lib().agpm_window_moments_dev(C.c_void_p(d_values_ptr), count, window, C.c_void_p(d_out_ptr),
                                          None if stream is None else C.c_void_p(stream)))
+
+
+STRATEGIES = {"auto": 0, "warp": 1, "lane": 2}
+
+
+def set_strategy(name):
+    """Sampler kernel choice (all draw identical samples): auto | warp | lane."""
+    _check(lib().agpm_ns_set_strategy(STRATEGIES[name]))
 
 
 def kernel_launches():

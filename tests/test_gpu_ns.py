@@ -36,9 +36,16 @@ def graphs(agpm):
     return _graphs(agpm)
 
 
+@pytest.fixture(params=["warp", "lane"])
+def strategy(agpm, request):
+    agpm.set_strategy(request.param)
+    yield request.param
+    agpm.set_strategy("auto")
+
+
 @pytest.mark.parametrize("name", ["er200", "er200_rel", "er60_dense", "rmat12_rel", "rmat12"])
 @pytest.mark.parametrize("pattern", PATTERNS)
-def test_draw_bit_exact(agpm, oracle, graphs, name, pattern):
+def test_draw_bit_exact(agpm, oracle, graphs, name, pattern, strategy):
     g = graphs[name]
     off, nbr = g.arrays()
     m = g.edge_count
@@ -53,7 +60,7 @@ def test_draw_bit_exact(agpm, oracle, graphs, name, pattern):
     np.testing.assert_array_equal(b, ob)
 
 
-def test_config1_first_2pow16_bit_exact(agpm, oracle):
+def test_config1_first_2pow16_bit_exact(agpm, oracle, strategy):
     """Config 1 graph (er_graph(10^4, 20/9999, 1), degree-relabelled), triangle,
     stream seed 1: the first 2^16 samples match record for record."""
     g = agpm.er_graph(10000, 20 / 9999, 1).relabel_by_degree()
@@ -66,7 +73,7 @@ def test_config1_first_2pow16_bit_exact(agpm, oracle):
     np.testing.assert_array_equal(b, ob)
 
 
-def test_fixed_budget_matches_oracle(agpm, oracle):
+def test_fixed_budget_matches_oracle(agpm, oracle, strategy):
     g = agpm.rmat(11, 16, seed=5).relabel_by_degree()
     off, nbr = g.arrays()
     plan = agpm.compile_plan("4clique")
@@ -79,7 +86,7 @@ def test_fixed_budget_matches_oracle(agpm, oracle):
 
 
 @pytest.mark.parametrize("pattern,eps", [("4clique", 0.05), ("triangle", 0.02), ("4cycle", 0.05)])
-def test_online_stops_where_oracle_stops(agpm, oracle, pattern, eps):
+def test_online_stops_where_oracle_stops(agpm, oracle, pattern, eps, strategy):
     g = agpm.rmat(11, 16, seed=7).relabel_by_degree()
     off, nbr = g.arrays()
     plan = agpm.compile_plan(pattern)
