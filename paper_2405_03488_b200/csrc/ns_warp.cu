@@ -34,14 +34,13 @@ constexpr int kWarpBatch = 8;  // sample ids claimed per cursor atomic
 __device__ __forceinline__ uint32_t kary_lb(const uint32_t* base, uint32_t lo, uint32_t hi, uint32_t x,
                                             int lane, bool* found) {
   while (hi - lo > 32) {
-    const uint32_t span = hi - lo;
-    const uint32_t pos = lo + (uint32_t)(((unsigned long long)(lane + 1) * span) / 33u);
-    const unsigned bal = __ballot_sync(FULL, ldn(base, pos) < x);
-    const int c = __popc(bal);
-    const uint32_t nlo = c ? lo + (uint32_t)(((unsigned long long)c * span) / 33u) + 1 : lo;
-    const uint32_t nhi = c < 32 ? lo + (uint32_t)(((unsigned long long)(c + 1) * span) / 33u) : hi;
+    // 32 probes at lo + (i+1)*step, step = floor(span/33) >= 1, all < hi
+    const uint32_t step = (hi - lo) / 33u;
+    const unsigned bal = __ballot_sync(FULL, ldn(base, lo + (uint32_t)(lane + 1) * step) < x);
+    const uint32_t c = __popc(bal);
+    const uint32_t nlo = c ? lo + c * step + 1 : lo;
+    hi = c < 32 ? lo + (c + 1) * step : hi;
     lo = nlo;
-    hi = nhi;
   }
   const uint32_t n = hi - lo;
   const uint32_t v = (uint32_t)lane < n ? ldn(base, lo + lane) : INF;
@@ -49,6 +48,19 @@ __device__ __forceinline__ uint32_t kary_lb(const uint32_t* base, uint32_t lo, u
   const unsigned eq = __ballot_sync(FULL, v == x && (uint32_t)lane < n);
   if (found) *found = eq != 0;
   return lo + __popc(lt);
+}
+
+// per-lane branchless lower_bound of a in base[0, n): the trip count depends
+// only on n (warp-uniform), so lanes never diverge
+__device__ __forceinline__ uint32_t lane_lb(const uint32_t* base, uint32_t n, uint32_t a) {
+  if (n == 0) return 0;
+  uint32_t b = 0;
+  while (n > 1) {
+    const uint32_t half = n >> 1;
+    b = ldn(base, b + half - 1) < a ? b + half : b;
+    n -= half;
+  }
+  return b + (ldn(base, b) < a ? 1u : 0u);
 }
 
 // b ascending across lanes (INF padded); does any lane hold a?
@@ -248,34 +260,27 @@ __global__ void __launch_bounds__(kThreads) ns_warp_kernel(const SampleLaunch L)
           const bool valid = i < dsize;
           const uint32_t a = valid ? ldn(nbr, dbase + i) : INF;
           const int last = (int)min(31u, dsize - 1 - ia);
-          const uint32_t a_first = __shfl_sync(FULL, a, 0);
           const uint32_t a_last = __shfl_sync(FULL, a, last);
           bool ok = valid;
 #pragma unroll
           for (int q = 0; q < K; ++q) {
             if (q < j && ((in_m >> q) & 1u) && q != drv) {
               const uint32_t* B = nbr + pb[q];
-              uint32_t c = cur[q];
+              const uint32_t c = cur[q];
               const uint32_t e = re[q];
               bool hit = false;
-              for (;;) {
-                if (c >= e) {  // list q exhausted: nothing from a_first on survives
-                  exhausted = true;
-                  hit = false;
-                  break;
-                }
+              if (c >= e) {  // list q exhausted: no driver element from here on matches
+                exhausted = true;
+              } else if (e - c <= 32) {  // whole remaining window in one coalesced chunk
                 const uint32_t b = c + lane < e ? ldn(B, c + lane) : INF;
-                const uint32_t bmax = __shfl_sync(FULL, b, 31);
-                if (bmax < a_first) {  // whole chunk below the window: jump
-                  c = kary_lb(B, c + 32, e, a_first, lane, nullptr);
-                  continue;
-                }
-                hit |= chunk_contains(b, a);
-                if (bmax >= a_last) break;
-                c += 32;
+                hit = chunk_contains(b, a);
+                cur[q] = c + __popc(__ballot_sync(FULL, b <= a_last));
+              } else {  // per-lane search; the cursor follows the chunk's last element
+                const uint32_t o = c + lane_lb(B + c, e - c, a);
+                hit = o < e && ldn(B, o) == a;
+                cur[q] = __shfl_sync(FULL, o, last);
               }
-              cur[q] = c;
-              ok = ok && hit && !exhausted;
+              ok = ok && hit;
             }
           }
 #pragma unroll
