@@ -33,6 +33,7 @@ constexpr int kWarpBatch = 8;  // sample ids claimed per cursor atomic
 // arguments, result uniform. `found` = (answer < hi && base[answer] == x).
 __device__ __forceinline__ uint32_t kary_lb(const uint32_t* base, uint32_t lo, uint32_t hi, uint32_t x,
                                             int lane, bool* found) {
+  const uint32_t end = hi;
   while (hi - lo > 32) {
     // 32 probes at lo + (i+1)*step, step = floor(span/33) >= 1, all < hi
     const uint32_t step = (hi - lo) / 33u;
@@ -44,10 +45,9 @@ __device__ __forceinline__ uint32_t kary_lb(const uint32_t* base, uint32_t lo, u
   }
   const uint32_t n = hi - lo;
   const uint32_t v = (uint32_t)lane < n ? ldn(base, lo + lane) : INF;
-  const unsigned lt = __ballot_sync(FULL, v < x);
-  const unsigned eq = __ballot_sync(FULL, v == x && (uint32_t)lane < n);
-  if (found) *found = eq != 0;
-  return lo + __popc(lt);
+  const uint32_t r = lo + __popc(__ballot_sync(FULL, v < x));
+  if (found) *found = r < end && ldn(base, r) == x;  // the answer may sit just past the last window
+  return r;
 }
 
 // per-lane branchless lower_bound of a in base[0, n): the trip count depends
