@@ -190,7 +190,8 @@ int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delt
 
 /* Sampler strategy: 0 = auto (default), 1 = one warp per sample
  * (k-ary searches + coalesced chunk intersections), 2 = one lane per sample
- * (tiny adjacency lists). All strategies draw identical samples. */
+ * (tiny adjacency lists), 3 = frontier phases (element-parallel
+ * intersections over a whole batch). All strategies draw identical samples. */
 int agpm_ns_set_strategy(int strategy);
 
 /* Device-pointer building blocks (bench / multi-rank driver): enqueue only.

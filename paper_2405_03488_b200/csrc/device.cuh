@@ -34,8 +34,8 @@ struct DeviceCtx {
   int sm_count = 0;
   cudaStream_t stream = nullptr;
   // grow-only scratch
-  void* scratch[8] = {nullptr};
-  size_t scratch_bytes[8] = {0};
+  void* scratch[12] = {nullptr};
+  size_t scratch_bytes[12] = {0};
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   void* get(int slot, size_t bytes);

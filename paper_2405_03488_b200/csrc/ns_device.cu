@@ -148,13 +148,14 @@ GraphArgs graph_args(const agpm_graph* g) {
 // Strategy: one warp per sample (coalesced chunk intersections, k-ary
 // searches) unless adjacency lists are tiny, where one lane per sample keeps
 // 32 samples in flight per warp. Override with agpm_ns_set_strategy().
-constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2;
+constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3;
 int g_strategy = kStrategyAuto;
 
-int choose_strategy(const agpm_graph* g) {
+int choose_strategy(const agpm_graph* g, uint64_t count) {
   if (g_strategy != kStrategyAuto) return g_strategy;
   const double avg_deg = g->n ? static_cast<double>(g->arcs) / g->n : 0.0;
-  return avg_deg <= 24.0 && g->max_degree <= 256 ? kStrategyLane : kStrategyWarp;
+  if (avg_deg <= 24.0 && g->max_degree <= 256) return kStrategyLane;
+  return count >= (1ull << 18) ? kStrategyFrontier : kStrategyWarp;
 }
 
 // enqueue one sampling launch for ids [first, first+count) into d_values
@@ -165,8 +166,11 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
   AGPM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
   SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};
   if (dp.k < 3 || dp.k > AGPM_MAX_K) throw std::invalid_argument("device sampler needs 3 <= k <= 9");
-  if (choose_strategy(g) == kStrategyLane)
+  const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, count);  // B_min replay: warp kernel
+  if (strat == kStrategyLane)
     launch_ns_lane(L, s);
+  else if (strat == kStrategyFrontier)
+    launch_ns_frontier(L, s);
   else
     launch_ns_warp(L, s);
 }
@@ -194,7 +198,8 @@ extern "C" {
 
 int agpm_ns_set_strategy(int strategy) {
   return guarded([&] {
-    if (strategy < 0 || strategy > 2) throw std::invalid_argument("strategy must be 0 (auto), 1 (warp) or 2 (lane)");
+    if (strategy < 0 || strategy > 3)
+      throw std::invalid_argument("strategy must be 0 (auto), 1 (warp), 2 (lane) or 3 (frontier)");
     g_strategy = strategy;
   });
 }

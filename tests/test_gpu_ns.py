@@ -36,7 +36,7 @@ def graphs(agpm):
     return _graphs(agpm)
 
 
-@pytest.fixture(params=["warp", "lane"])
+@pytest.fixture(params=["warp", "lane", "frontier"])
 def strategy(agpm, request):
     agpm.set_strategy(request.param)
     yield request.param
