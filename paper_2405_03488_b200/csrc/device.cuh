@@ -36,10 +36,10 @@ struct DeviceCtx {
   // grow-only scratch
   void* scratch[12] = {nullptr};
   size_t scratch_bytes[12] = {0};
-  void* pinned = nullptr;
-  size_t pinned_bytes = 0;
+  void* pinned[4] = {nullptr};
+  size_t pinned_bytes[4] = {0};
   void* get(int slot, size_t bytes);
-  void* get_pinned(size_t bytes);
+  void* get_pinned(int slot, size_t bytes);
 };
 
 DeviceCtx& ctx_for_current_device();

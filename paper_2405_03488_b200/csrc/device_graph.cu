@@ -39,13 +39,13 @@ void* DeviceCtx::get(int slot, size_t bytes) {
   return scratch[slot];
 }
 
-void* DeviceCtx::get_pinned(size_t bytes) {
-  if (pinned_bytes < bytes) {
-    if (pinned) AGPM_CUDA(cudaFreeHost(pinned));
-    AGPM_CUDA(cudaMallocHost(&pinned, bytes));
-    pinned_bytes = bytes;
+void* DeviceCtx::get_pinned(int slot, size_t bytes) {
+  if (pinned_bytes[slot] < bytes) {
+    if (pinned[slot]) AGPM_CUDA(cudaFreeHost(pinned[slot]));
+    AGPM_CUDA(cudaMallocHost(&pinned[slot], bytes));
+    pinned_bytes[slot] = bytes;
   }
-  return pinned;
+  return pinned[slot];
 }
 
 DeviceCtx& ctx_for_current_device() {

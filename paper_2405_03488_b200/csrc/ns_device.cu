@@ -277,7 +277,7 @@ int agpm_ns_fixed_budget(agpm_graph* g, const agpm_plan* plan, uint64_t budget, 
     const uint64_t nwin_chunk = (chunk + kWin - 1) / kWin;
     auto* d_values = static_cast<double*>(ctx.get(1, sizeof(double) * chunk));
     auto* d_win = static_cast<agpm_accumulator*>(ctx.get(4, sizeof(agpm_accumulator) * nwin_chunk));
-    auto* h_win = static_cast<agpm_accumulator*>(ctx.get_pinned(sizeof(agpm_accumulator) * nwin_chunk));
+    auto* h_win = static_cast<agpm_accumulator*>(ctx.get_pinned(0, sizeof(agpm_accumulator) * nwin_chunk));
     agpm_accumulator acc{0, 0, 0.0, 0.0};
     for (uint64_t done = 0; done < budget; done += chunk) {
       const uint64_t c = std::min(chunk, budget - done);
@@ -320,7 +320,7 @@ int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delt
     auto* d_values = static_cast<double*>(ctx.get(1, sizeof(double) * max_batch));
     auto* d_win = static_cast<agpm_accumulator*>(ctx.get(4, sizeof(agpm_accumulator) * (max_batch / window + 1)));
     auto* d_state = static_cast<OnlineState*>(ctx.get(5, sizeof(OnlineState)));
-    auto* h_state = static_cast<OnlineState*>(ctx.get_pinned(sizeof(OnlineState)));
+    auto* h_state = static_cast<OnlineState*>(ctx.get_pinned(1, sizeof(OnlineState)));
     AGPM_CUDA(cudaMemsetAsync(d_state, 0, sizeof(OnlineState), s));
     auto t0 = std::chrono::steady_clock::now();
     uint64_t launched = 0;

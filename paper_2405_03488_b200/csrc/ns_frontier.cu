@@ -523,7 +523,7 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
   A.offsets = reinterpret_cast<unsigned long long*>(slab + o_off);
   A.desc = slab + o_desc;
   void* tmp = slab + o_tmp;
-  auto* h_total = static_cast<unsigned long long*>(ctx.get_pinned(64));
+  auto* h_total = static_cast<unsigned long long*>(ctx.get_pinned(2, 64));
 
   const int sms = ctx.sm_count;
   for (unsigned long long done = 0; done < L.count; done += cap) {
