@@ -273,10 +273,16 @@ def run_gpu(args):
     if dist is not None:
         dist.barrier()
     t = time.perf_counter()
+    up_s = run_s = 0.0
     for s in range(e2e_steps):
+        t1 = time.perf_counter()
         dgh = A.DeviceGraph(g)
+        t2 = time.perf_counter()
         acc = A.run_fixed_budget(dgh, plan, B, 1 + s * world + rank)
+        t3 = time.perf_counter()
         del dgh
+        up_s += t2 - t1
+        run_s += t3 - t2
     e2e_s = time.perf_counter() - t
     if dist is not None:
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -325,7 +331,8 @@ def run_gpu(args):
                                         "device_bytes": info["device_bytes"], "gen_s": round(gen_s, 2)}),
             "time_to_converge": ttc,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "what": "DeviceGraph(host CSR) upload + run_fixed_budget(2^24) + accumulator read-back"},
+                    "what": "DeviceGraph(host CSR) upload + run_fixed_budget(2^24) + accumulator read-back",
+                    "upload_s_per_step": up_s / e2e_steps, "sampling_s_per_step": run_s / e2e_steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bmin_bytes_per_sample": bmin_per_sample, "kernel_ms": kern_ms,

@@ -1,0 +1,21 @@
+"""Developer tool: sample 2^24 ids of the bench workload through one strategy (for ncu)."""
+import os, sys, time
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_2405_03488_b200 as A
+strategy = sys.argv[1] if len(sys.argv) > 1 else "frontier"
+pattern = sys.argv[2] if len(sys.argv) > 2 else "4clique"
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+g = A.rmat(20, 16, seed=1).relabel_by_degree()
+dg = A.DeviceGraph(g)
+plan = A.compile_plan(pattern)
+A.set_strategy(strategy)
+B = 1 << 24
+vals = torch.empty(B, dtype=torch.float64, device="cuda")
+st = torch.cuda.Stream(); torch.cuda.set_stream(st)
+for r in range(reps):
+    torch.cuda.synchronize(); t = time.perf_counter()
+    A.sample_dev(dg, plan, 1, r * B, B, vals.data_ptr(), st.cuda_stream)
+    torch.cuda.synchronize(); dt = time.perf_counter() - t
+    print(f"{strategy} {pattern} rep {r}: {dt*1e3:.2f} ms  {B/dt:.3e} samples/s  hits {(vals != 0).float().mean().item():.4f}")
