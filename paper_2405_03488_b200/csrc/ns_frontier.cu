@@ -7,15 +7,18 @@
 //            the seed arc index, the previous pick's index), single-list steps
 //            resolved inline by index arithmetic, driver = smallest range;
 //            writes an IsectDesc + |driver| for the next multi-list step.
-//   scan     (CUB)                  exclusive scan of |driver| -> element offsets.
-//   isect    (1 lane / element)     every driver element of every sample is one
-//            lane: load-balanced sample lookup, coalesced driver loads, one
-//            branchless lower_bound per other list -> hit bit (ballot -> one
-//            32-bit bitmap word per warp step). No per-sample serial work and
-//            no idle lanes however skewed the list lengths are.
-//   pick     (1 thread / sample)    popcount of the sample's bit range minus
-//            bound vertices = |S_j|, r = next_below(|S_j|), r-th set bit ->
-//            v_j, alpha *= |S_j|, then `advance` to the next step.
+//   scan     (CUB)                  one exclusive scan of packed (bitmap words,
+//            merge segments) per sample -> word-aligned bitmap slots + work offsets.
+//   isect    (1 thread / segment)   merge-path intersection: the merge of the
+//            driver D with each other list B is cut into fixed SEG-step
+//            segments; a thread finds its start on the merge diagonal with one
+//            binary search, then merges SEG steps, marking D elements absent
+//            from B (present, for out-lists) in the sample's fail bitmap.
+//            Equal-sized segments keep SIMT lanes busy however skewed the list
+//            lengths are; pairs with |B| > 32|D| use per-element search instead.
+//   pick     (1 thread / sample)    |S_j| = |D| - fails - bound vertices,
+//            r = next_below(|S_j|), r-th surviving bit -> v_j, alpha *= |S_j|,
+//            then `advance` to the next step.
 //
 // Candidate sets and picks are exactly build_step_candidates +
 // cand[next_below(|cand|)] (walker.hpp:30-83, ns_engine.cpp:27-53) with the
@@ -33,17 +36,24 @@ namespace agpm_b200 {
 namespace {
 
 constexpr uint32_t INF = 0xffffffffu;
-constexpr int kMaxOther = AGPM_MAX_K - 2;
 
+constexpr uint32_t SEG = 64;        // merge steps per isect thread
+constexpr uint32_t SEG_SEARCH = 16; // driver elements per thread in search mode
+constexpr uint32_t kSearchRatio = 32;  // |B| > 32 |D|: search instead of merge (set_ops.hpp:13)
+
+// Per-sample intersection job, slots indexed by matching position (static indexing).
 template <int K>
 struct __align__(16) IsectDesc {
-  unsigned long long drv;               // absolute index of the driver range start
-  unsigned long long start[K - 2];      // other lists (in-lists restricted, out-lists whole)
-  uint32_t len[K - 2];
-  uint32_t n_other;
-  uint32_t out_slots;                   // bit t set: slot t is an out-list (difference)
-  uint32_t drv_pos;                     // matching position owning the driver list
-  uint32_t drv_rs;                      // driver range start relative to that list
+  unsigned long long drv;             // absolute index of the driver range start
+  unsigned long long start[K - 1];    // other lists: in-lists restricted, out-lists whole
+  uint32_t len[K - 1];
+  uint32_t nseg[K - 1];               // isect work items for this list
+  uint32_t dsize;
+  uint32_t lists;                     // bit q: position q is an "other" list
+  uint32_t outs;                      // bit q: ... and it is an out-list (difference)
+  uint32_t search;                    // bit q: ... and it runs in search mode
+  uint32_t drv_pos;                   // matching position owning the driver list
+  uint32_t drv_rs;                    // driver range start relative to that list
 };
 
 struct FrontierArgs {
@@ -58,8 +68,8 @@ struct FrontierArgs {
   uint32_t* bnd;            // K * cap
   uint32_t* hbo;            // K * cap, hint: lower_bound(hbl) = hbo (relative)
   uint32_t* hbl;            // K * cap
-  uint32_t* dsize;          // cap + 1 (|driver| of the pending step, 0 = not pending)
-  unsigned long long* offsets;  // cap + 1
+  unsigned long long* work;     // cap + 1: (bitmap words << 32 | segments), 0 = not pending
+  unsigned long long* offsets;  // cap + 1: exclusive scan of work
   void* desc;               // IsectDesc<K>[cap]
   uint32_t* bitmap;
   // outputs
@@ -178,7 +188,7 @@ __device__ void load_state(const FrontierArgs& A, unsigned long long i, Sample<K
 template <int K>
 __device__ void finish(const FrontierArgs& A, unsigned long long i, const Sample<K>& S, int nb, bool hit) {
   A.values[i] = hit ? S.alpha : 0.0;
-  A.dsize[i] = 0;
+  A.work[i] = 0;
   if (A.bindings) {
 #pragma unroll
     for (int q = 0; q < K; ++q) A.bindings[i * K + q] = q < nb ? S.bnd[q] : INF;
@@ -278,32 +288,36 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
       bind(S, j, pick);
       continue;
     }
-    // multi-list step: hand the intersection to the element-parallel phase
+    // multi-list step: hand the intersection to the merge-path phase
     IsectDesc<K> d;
     d.drv = dbase;
-    uint32_t t = 0, outs = 0;
+    d.dsize = dsize;
+    d.lists = d.outs = d.search = 0;
+    uint32_t segs = 0;
 #pragma unroll
-    for (int q = 0; q < K; ++q) {
-      if (q < j && q != drv && (((in_m | out_m) >> q) & 1u) && t < K - 2) {
+    for (int q = 0; q < K - 1; ++q) {
+      d.start[q] = 0;
+      d.len[q] = 0;
+      d.nseg[q] = 0;
+      if (q < j && q != drv && (((in_m | out_m) >> q) & 1u)) {
         const bool is_out = (out_m >> q) & 1u;
-        d.start[t] = is_out ? S.pb[q] : S.pb[q] + rs[q];
-        d.len[t] = is_out ? S.pd[q] : re[q] - rs[q];
-        if (is_out) outs |= 1u << t;
-        ++t;
+        d.start[q] = is_out ? S.pb[q] : S.pb[q] + rs[q];
+        d.len[q] = is_out ? S.pd[q] : re[q] - rs[q];
+        d.lists |= 1u << q;
+        if (is_out) d.outs |= 1u << q;
+        if (d.len[q] / kSearchRatio > dsize) {
+          d.search |= 1u << q;
+          d.nseg[q] = (dsize + SEG_SEARCH - 1) / SEG_SEARCH;
+        } else {
+          d.nseg[q] = (dsize + d.len[q] + SEG - 1) / SEG;
+        }
+        segs += d.nseg[q];
       }
     }
-#pragma unroll
-    for (int u = 0; u < K - 2; ++u)
-      if (u >= (int)t) {
-        d.start[u] = 0;
-        d.len[u] = 0;
-      }
-    d.n_other = t;
-    d.out_slots = outs;
     d.drv_pos = (uint32_t)drv;
     d.drv_rs = dbase_rel(S, drv, rs);
     reinterpret_cast<IsectDesc<K>*>(A.desc)[i] = d;
-    A.dsize[i] = dsize;
+    A.work[i] = ((unsigned long long)((dsize + 31) >> 5) << 32) | segs;
     store_state(A, i, S, j);
     return;
   }
@@ -350,61 +364,106 @@ __global__ void __launch_bounds__(256) fr_seed_kernel(const FrontierArgs A) {
   }
 }
 
-// One lane per driver element; warps walk contiguous runs of bitmap words.
+__device__ __forceinline__ void flush_bits(uint32_t* words, uint32_t w, uint32_t bits) {
+  if (bits) atomicOr(words + w, bits);
+}
+
+// One thread per work item (merge segment or search batch); a warp covers a
+// contiguous run of items, so the owning sample is found by one k-ary search
+// over the scanned offsets and then advanced linearly.
 template <int K>
 __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, unsigned long long total) {
   const int lane = threadIdx.x & 31;
-  const unsigned long long words = (total + 31) >> 5;
-  const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
-  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-  const unsigned long long per = (words + nwarps - 1) / nwarps;
-  const unsigned long long w0 = warp * per, w1 = min(words, w0 + per);
-  if (w0 >= w1) return;
   const unsigned long long* __restrict__ off = A.offsets;
   const IsectDesc<K>* __restrict__ desc = reinterpret_cast<const IsectDesc<K>*>(A.desc);
   const uint32_t* __restrict__ nbr = A.g.nbr;
-  // sample holding element 32*w0: last s with off[s] <= 32*w0 (k-ary over the offsets)
-  unsigned long long s_cur;
-  {
-    const unsigned long long e0 = w0 * 32;
-    unsigned long long lo = 0, hi = A.count;  // answer in [lo, hi)
-    while (hi - lo > 32) {
-      const unsigned long long step = (hi - lo) / 33;
-      const unsigned long long pos = lo + (unsigned long long)(lane + 1) * step;
-      const unsigned bal = __ballot_sync(FULL, off[pos] <= e0);
-      const unsigned c = __popc(bal);
-      const unsigned long long nlo = c ? lo + c * step : lo;
-      hi = c < 32 ? lo + (c + 1) * step : hi;
-      lo = nlo;
+  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  for (unsigned long long base = ((blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5) * 32;
+       base < total; base += nwarps * 32) {
+    // sample of item `base`: last s with seg_off[s] <= base
+    unsigned long long s;
+    {
+      unsigned long long lo = 0, hi = A.count;
+      while (hi - lo > 32) {
+        const unsigned long long step = (hi - lo) / 33;
+        const unsigned long long pos = lo + (unsigned long long)(lane + 1) * step;
+        const unsigned c = __popc(__ballot_sync(FULL, (off[pos] & 0xffffffffull) <= base));
+        const unsigned long long nlo = c ? lo + c * step : lo;
+        hi = c < 32 ? lo + (c + 1) * step : hi;
+        lo = nlo;
+      }
+      const unsigned long long pos = lo + lane;
+      const bool le = pos < hi && (off[pos] & 0xffffffffull) <= base;
+      s = lo + __popc(__ballot_sync(FULL, le)) - 1;
     }
-    const unsigned long long pos = lo + lane;
-    const bool le = pos < hi && off[pos] <= e0;
-    s_cur = lo + __popc(__ballot_sync(FULL, le)) - 1;
-  }
-  for (unsigned long long w = w0; w < w1; ++w) {
-    const unsigned long long e = w * 32 + lane;
-    const bool valid = e < total;
-    unsigned long long s = s_cur;
-    if (valid)
-      while (off[s + 1] <= e) ++s;
-    bool ok = false;
-    if (valid) {
-      const IsectDesc<K> d = desc[s];
-      const uint32_t a = ldn(nbr, d.drv + (e - off[s]));
-      ok = true;
+    const unsigned long long g = base + lane;
+    if (g >= total) continue;
+    while ((off[s + 1] & 0xffffffffull) <= g) ++s;
+    const IsectDesc<K>& d = desc[s];  // fields read straight from L1, no local copy
+    uint32_t l = (uint32_t)(g - (off[s] & 0xffffffffull));
+    uint32_t* words = A.bitmap + (off[s] >> 32);
+    const uint32_t* D = nbr + d.drv;
+    const uint32_t nd = d.dsize;
 #pragma unroll
-      for (int t = 0; t < K - 2; ++t) {
-        if ((uint32_t)t < d.n_other) {
-          const uint32_t* B = nbr + d.start[t];
-          const uint32_t o = lb_branchless(B, d.len[t], a);
-          const bool found = o < d.len[t] && ldn(B, o) == a;
-          ok = ok && (((d.out_slots >> t) & 1u) ? !found : found);
+    for (int q = 0; q < K - 1; ++q) {
+      if (!((d.lists >> q) & 1u)) continue;
+      if (l >= d.nseg[q]) {
+        l -= d.nseg[q];
+        continue;
+      }
+      const uint32_t* B = nbr + d.start[q];
+      const uint32_t nb = d.len[q];
+      const bool is_out = (d.outs >> q) & 1u;
+      uint32_t cw = 0xffffffffu, acc = 0;
+      if ((d.search >> q) & 1u) {
+        const uint32_t i0 = l * SEG_SEARCH, i1 = min(nd, i0 + SEG_SEARCH);
+        for (uint32_t i = i0; i < i1; ++i) {
+          const uint32_t x = ldn(D, i);
+          uint32_t lo = 0, hi = nb;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (ldn(B, mid) < x) lo = mid + 1; else hi = mid;
+          }
+          const bool found = lo < nb && ldn(B, lo) == x;
+          if ((i >> 5) != cw) {
+            if (cw != 0xffffffffu) flush_bits(words, cw, acc);
+            cw = i >> 5;
+            acc = 0;
+          }
+          if (found == is_out) acc |= 1u << (i & 31);
+        }
+      } else {
+        // merge-path: start of segment l on diagonal dg (D first on ties)
+        const uint32_t dg = l * SEG;
+        uint32_t lo = dg > nb ? dg - nb : 0, hi = min(dg, nd);
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (ldn(D, mid) <= ldn(B, dg - 1 - mid)) lo = mid + 1; else hi = mid;
+        }
+        uint32_t i = lo, jb = dg - lo;
+        const uint32_t steps = min(SEG, nd + nb - dg);
+        uint32_t x = i < nd ? ldn(D, i) : INF;
+        uint32_t y = jb < nb ? ldn(B, jb) : INF;
+        for (uint32_t t = 0; t < steps; ++t) {
+          if (i < nd && x <= y) {  // consume D[i]: B[jb] = lower_bound(B, D[i])
+            const bool found = x == y;
+            if ((i >> 5) != cw) {
+              if (cw != 0xffffffffu) flush_bits(words, cw, acc);
+              cw = i >> 5;
+              acc = 0;
+            }
+            if (found == is_out) acc |= 1u << (i & 31);
+            ++i;
+            x = i < nd ? ldn(D, i) : INF;
+          } else {
+            ++jb;
+            y = jb < nb ? ldn(B, jb) : INF;
+          }
         }
       }
+      if (cw != 0xffffffffu) flush_bits(words, cw, acc);
+      break;
     }
-    const unsigned bal = __ballot_sync(FULL, ok);
-    if (lane == 0) A.bitmap[w] = bal;
-    s_cur = __shfl_sync(FULL, s, 31);  // lane 31 holds the largest sample of this word
   }
 }
 
@@ -413,66 +472,56 @@ __global__ void __launch_bounds__(256) fr_pick_kernel(const FrontierArgs A, int 
   const uint32_t* __restrict__ nbr = A.g.nbr;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < A.count;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint32_t dsize = A.dsize[i];
-    if (dsize == 0) continue;
+    if (A.work[i] == 0) continue;
     const int j = s_step + 2;
     Sample<K> S(A.seed, A.first_id + i);
     load_state(A, i, S, j);
     const IsectDesc<K> d = reinterpret_cast<const IsectDesc<K>*>(A.desc)[i];
-    const unsigned long long off = A.offsets[i];
-    // order bounds of this step (bound vertices outside them cannot be candidates)
+    const uint32_t dsize = d.dsize;
+    const uint32_t* words = A.bitmap + (A.offsets[i] >> 32);
     uint32_t lo = 0, hi = INF;
 #pragma unroll
     for (int q = 0; q < K; ++q) {
       if (q < j && ((A.p.gt_mask[s_step] >> q) & 1u)) lo = max(lo, S.bnd[q] + 1);
       if (q < j && ((A.p.lt_mask[s_step] >> q) & 1u)) hi = min(hi, S.bnd[q]);
     }
-    // bound vertices that survived the intersection are not candidates
+    // bound vertices that survived the intersection are not candidates (walker.hpp:70-82)
     uint32_t ex[K];
 #pragma unroll
     for (int q = 0; q < K; ++q) {
       ex[q] = INF;
       if (q < j && S.bnd[q] >= lo && S.bnd[q] < hi) {
         const uint32_t o = lb_thread(nbr + d.drv, 0, dsize, S.bnd[q]);
-        if (o < dsize && ldn(nbr, d.drv + o) == S.bnd[q]) {
-          const unsigned long long bit = off + o;
-          if ((A.bitmap[bit >> 5] >> (bit & 31)) & 1u) ex[q] = o;
-        }
+        if (o < dsize && ldn(nbr, d.drv + o) == S.bnd[q] && !((words[o >> 5] >> (o & 31)) & 1u)) ex[q] = o;
       }
     }
-    auto word_at = [&](unsigned long long w) -> unsigned {
-      unsigned m = A.bitmap[w];
-      const unsigned long long b0 = w * 32;
-      if (b0 < off) m &= ~0u << (off - b0);
-      const unsigned long long end = off + dsize;
-      if (b0 + 32 > end) m &= end - b0 >= 32 ? ~0u : ((1u << (end - b0)) - 1u);
+    const uint32_t nw = (dsize + 31) >> 5;
+    auto live = [&](uint32_t w) -> unsigned {  // surviving candidates in word w
+      unsigned m = ~words[w];
+      if (w == nw - 1 && (dsize & 31)) m &= (1u << (dsize & 31)) - 1u;
 #pragma unroll
       for (int q = 0; q < K; ++q)
-        if (ex[q] != INF) {
-          const unsigned long long bit = off + ex[q];
-          if ((bit >> 5) == w) m &= ~(1u << (bit & 31));
-        }
+        if (ex[q] != INF && (ex[q] >> 5) == w) m &= ~(1u << (ex[q] & 31));
       return m;
     };
-    const unsigned long long wa = off >> 5, wb = (off + dsize - 1) >> 5;
     unsigned long long cnt = 0;
-    for (unsigned long long w = wa; w <= wb; ++w) cnt += __popc(word_at(w));
+    for (uint32_t w = 0; w < nw; ++w) cnt += __popc(live(w));
     if (cnt == 0) {
       finish(A, i, S, j, false);
       continue;
     }
     unsigned long long r = S.rng.next_below(cnt);
     uint32_t o = 0;
-    for (unsigned long long w = wa; w <= wb; ++w) {
-      const unsigned m = word_at(w);
+    for (uint32_t w = 0; w < nw; ++w) {
+      const unsigned m = live(w);
       const unsigned pc = __popc(m);
       if (r < pc) {
-        o = (uint32_t)(w * 32 + __fns(m, 0, (int)r + 1) - off);
+        o = w * 32 + __fns(m, 0, (int)r + 1);
         break;
       }
       r -= pc;
     }
-    S.alpha = __dmul_rn(S.alpha, (double)cnt);
+    S.alpha = __dmul_rn(S.alpha, (double)cnt);  // alpha *= |S_j| (ns_engine.cpp:39)
     const uint32_t pick = ldn(nbr, d.drv + o);
     // the pick sits at drv_rs + o in the driver's list: lower_bound(pick+1) = drv_rs + o + 1
 #pragma unroll
@@ -499,7 +548,6 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
   }
   const unsigned long long cap = std::min<unsigned long long>(L.count, 1ull << 22);
   A.cap = cap;
-  // state slab in scratch slot 6
   size_t bytes = 0;
   auto carve = [&](size_t n) {
     size_t at = (bytes + 255) & ~size_t(255);
@@ -507,11 +555,11 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
     return at;
   };
   const size_t o_ctr = carve(8 * cap), o_alpha = carve(8 * cap), o_bnd = carve(4ull * K * cap),
-               o_hbo = carve(4ull * K * cap), o_hbl = carve(4ull * K * cap), o_dsize = carve(4 * (cap + 1)),
+               o_hbo = carve(4ull * K * cap), o_hbl = carve(4ull * K * cap), o_work = carve(8 * (cap + 1)),
                o_off = carve(8 * (cap + 1)), o_desc = carve(sizeof(IsectDesc<K>) * cap);
   size_t scan_tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (const uint32_t*)nullptr, (unsigned long long*)nullptr,
-                                (int64_t)cap + 1, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (const unsigned long long*)nullptr,
+                                (unsigned long long*)nullptr, (int64_t)cap + 1, s);
   const size_t o_tmp = carve(scan_tmp + 256);
   char* slab = static_cast<char*>(ctx.get(9, bytes));
   A.ctr = reinterpret_cast<unsigned long long*>(slab + o_ctr);
@@ -519,7 +567,7 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
   A.bnd = reinterpret_cast<uint32_t*>(slab + o_bnd);
   A.hbo = reinterpret_cast<uint32_t*>(slab + o_hbo);
   A.hbl = reinterpret_cast<uint32_t*>(slab + o_hbl);
-  A.dsize = reinterpret_cast<uint32_t*>(slab + o_dsize);
+  A.work = reinterpret_cast<unsigned long long*>(slab + o_work);
   A.offsets = reinterpret_cast<unsigned long long*>(slab + o_off);
   A.desc = slab + o_desc;
   void* tmp = slab + o_tmp;
@@ -538,17 +586,17 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
     AGPM_CUDA(cudaGetLastError());
     for (int st = 0; st < K - 2; ++st) {
       if (!A.step_multi[st]) continue;
-      AGPM_CUDA(cudaMemsetAsync(A.dsize + c, 0, 4, s));
+      AGPM_CUDA(cudaMemsetAsync(A.work + c, 0, 8, s));
       size_t tb = scan_tmp;
-      AGPM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, A.dsize, A.offsets, (int64_t)c + 1, s));
+      AGPM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, A.work, A.offsets, (int64_t)c + 1, s));
       AGPM_CUDA(cudaMemcpyAsync(h_total, A.offsets + c, 8, cudaMemcpyDeviceToHost, s));
       AGPM_CUDA(cudaStreamSynchronize(s));
-      const unsigned long long total = *h_total;
-      if (total) {
-        const unsigned long long words = (total + 31) >> 5;
+      const unsigned long long words = *h_total >> 32, segs = *h_total & 0xffffffffull;
+      if (words) {
         A.bitmap = static_cast<uint32_t*>(ctx.get(8, 4 * words + 64));
-        const unsigned long long warps = std::min<unsigned long long>((words + 3) / 4, (unsigned long long)sms * 64);
-        fr_isect_kernel<K><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(A, total);
+        AGPM_CUDA(cudaMemsetAsync(A.bitmap, 0, 4 * words, s));
+        const unsigned long long warps = std::min<unsigned long long>((segs + 31) / 32, (unsigned long long)sms * 64);
+        fr_isect_kernel<K><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(A, segs);
         count_launch();
         AGPM_CUDA(cudaGetLastError());
       }
