@@ -37,7 +37,7 @@ namespace {
 
 constexpr uint32_t INF = 0xffffffffu;
 
-constexpr uint32_t SEG = 64;        // merge steps per isect thread
+constexpr uint32_t SEG = 64;        // merge steps per isect thread (<= 96: 128-bit mark window)
 constexpr uint32_t SEG_SEARCH = 16; // driver elements per thread in search mode
 constexpr uint32_t kSearchRatio = 32;  // |B| > 32 |D|: search instead of merge (set_ops.hpp:13)
 
@@ -444,22 +444,30 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
         const uint32_t steps = min(SEG, nd + nb - dg);
         uint32_t x = i < nd ? ldn(D, i) : INF;
         uint32_t y = jb < nb ? ldn(B, jb) : INF;
+        // branchless merge: every lane executes the same instruction stream;
+        // marks go to a 128-bit window starting at i's word (SEG <= 96 bits past it)
+        const uint32_t wbase = i >> 5;
+        unsigned long long m0 = 0, m1 = 0;
         for (uint32_t t = 0; t < steps; ++t) {
-          if (i < nd && x <= y) {  // consume D[i]: B[jb] = lower_bound(B, D[i])
-            const bool found = x == y;
-            if ((i >> 5) != cw) {
-              if (cw != 0xffffffffu) flush_bits(words, cw, acc);
-              cw = i >> 5;
-              acc = 0;
-            }
-            if (found == is_out) acc |= 1u << (i & 31);
-            ++i;
-            x = i < nd ? ldn(D, i) : INF;
-          } else {
-            ++jb;
-            y = jb < nb ? ldn(B, jb) : INF;
-          }
+          const bool take_d = x <= y;  // D first on ties: y = lower_bound(B, x) when D[i] is consumed
+          const bool mark = take_d && ((x == y) == is_out);
+          const uint32_t p = i - (wbase << 5);
+          m0 |= (unsigned long long)(mark && p < 64) << (p & 63);
+          m1 |= (unsigned long long)(mark && p >= 64) << (p & 63);
+          i += take_d;
+          jb += !take_d;
+          const uint32_t k = take_d ? i : jb;
+          const uint32_t lim = take_d ? nd : nb;
+          const uint32_t* src = take_d ? D : B;
+          const uint32_t v = k < lim ? ldn(src, k) : INF;
+          x = take_d ? v : x;
+          y = take_d ? y : v;
         }
+        flush_bits(words, wbase, (uint32_t)m0);
+        flush_bits(words, wbase + 1, (uint32_t)(m0 >> 32));
+        flush_bits(words, wbase + 2, (uint32_t)m1);
+        flush_bits(words, wbase + 3, (uint32_t)(m1 >> 32));
+        break;
       }
       if (cw != 0xffffffffu) flush_bits(words, cw, acc);
       break;
