@@ -2,28 +2,32 @@
 //
 // A batch of samples advances through the plan one multi-list step at a time:
 //
-//   advance  (1 thread / sample)   seed draw, bound-restricted ranges of the
+//   advance  (1 thread / sample)   seed draw; bound-restricted ranges of the
 //            step's lists (per-thread lower_bound narrowed by hints: vtx.up,
-//            the seed arc index, the previous pick's index), single-list steps
-//            resolved inline by index arithmetic, driver = smallest range;
-//            writes an IsectDesc + |driver| for the next multi-list step.
-//   scan     (CUB)                  one exclusive scan of packed (bitmap words,
-//            merge segments) per sample -> word-aligned bitmap slots + work offsets.
-//   isect    (1 thread / segment)   merge-path intersection: the merge of the
-//            driver D with each other list B is cut into fixed SEG-step
-//            segments; a thread finds its start on the merge diagonal with one
-//            binary search, then merges SEG steps, marking D elements absent
-//            from B (present, for out-lists) in the sample's fail bitmap.
-//            Equal-sized segments keep SIMT lanes busy however skewed the list
-//            lengths are; pairs with |B| > 32|D| use per-element search instead.
+//            the seed arc index, the previous pick's index); single-list steps
+//            resolved inline by index arithmetic; driver = smallest range;
+//            writes an IsectDesc and the sample's bitmap word count.
+//   scan     (CUB)                  word offsets: every sample's hit bitmap
+//            starts on a 32-bit word boundary.
+//   isect    (1 warp / bitmap word) a word = 32 driver elements of ONE sample.
+//            Per other list the warp loads 32 splitters in one coalesced load,
+//            each lane finds its bucket with a 5-step shuffle search and
+//            finishes with a ~3-level per-lane search (lists <= 32 elements:
+//            one load + shuffle membership). One ballot -> the fail word. No
+//            atomics, no memset, every lane busy whatever the skew.
 //   pick     (1 thread / sample)    |S_j| = |D| - fails - bound vertices,
-//            r = next_below(|S_j|), r-th surviving bit -> v_j, alpha *= |S_j|,
-//            then `advance` to the next step.
+//            r = next_below(|S_j|), r-th surviving bit -> v_j, alpha *= |S_j|.
+//            Nested reuse: when step j+1's lists contain step j's (cliques),
+//            S_{j+1} = {x in S_j : x in [lo', hi'), x != v_j} ∩ (new lists) —
+//            the survivors are compacted (warp-aggregated allocation) and become
+//            the next driver, so step j+1 intersects a handful of elements
+//            with ONE new list instead of re-intersecting all of them.
 //
 // Candidate sets and picks are exactly build_step_candidates +
 // cand[next_below(|cand|)] (walker.hpp:30-83, ns_engine.cpp:27-53) with the
-// sample's own CounterRng(seed, 0, id), so results are bit-identical to the
-// warp/lane kernels and to the reference's draw_sample with workers = 1.
+// sample's own CounterRng(seed, 0, id): the set S_j does not depend on how it
+// is computed, so results are bit-identical to the warp/lane kernels and to the
+// reference's draw_sample with workers = 1.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -36,23 +40,18 @@ namespace agpm_b200 {
 namespace {
 
 constexpr uint32_t INF = 0xffffffffu;
+constexpr uint32_t NO_DRV = 0xffffffffu;
 
-constexpr uint32_t SEG = 64;        // merge steps per isect thread (<= 96: 128-bit mark window)
-constexpr uint32_t SEG_SEARCH = 16; // driver elements per thread in search mode
-constexpr uint32_t kSearchRatio = 32;  // |B| > 32 |D|: search instead of merge (set_ops.hpp:13)
-
-// Per-sample intersection job, slots indexed by matching position (static indexing).
+// Per-sample intersection job; other-list slots are indexed by matching position.
 template <int K>
 struct __align__(16) IsectDesc {
-  unsigned long long drv;             // absolute index of the driver range start
+  const uint32_t* drv;                // driver list (adjacency range or compacted survivors)
   unsigned long long start[K - 1];    // other lists: in-lists restricted, out-lists whole
   uint32_t len[K - 1];
-  uint32_t nseg[K - 1];               // isect work items for this list
   uint32_t dsize;
-  uint32_t lists;                     // bit q: position q is an "other" list
-  uint32_t outs;                      // bit q: ... and it is an out-list (difference)
-  uint32_t search;                    // bit q: ... and it runs in search mode
-  uint32_t drv_pos;                   // matching position owning the driver list
+  uint32_t lists;                     // bit q: position q is an other list
+  uint32_t outs;                      // bit q: ... and an out-list (difference)
+  uint32_t drv_pos;                   // position owning the driver list, NO_DRV for survivors
   uint32_t drv_rs;                    // driver range start relative to that list
 };
 
@@ -60,18 +59,22 @@ struct FrontierArgs {
   GraphArgs g;
   DevPlan p;
   unsigned long long seed, first_id, count;
-  int step_multi[AGPM_MAX_K - 2];  // 1 if step s needs the intersection phase
+  int step_multi[AGPM_MAX_K - 2];  // step s needs the intersection phase
+  int step_reuse[AGPM_MAX_K - 2];  // step s reuses step s-1's survivors as its driver
   // per-sample state (SoA, stride cap)
   unsigned long long cap;
-  unsigned long long* ctr;  // rng counter (key re-derived from the id)
-  double* alpha;            // running scale; 0 once dead
-  uint32_t* bnd;            // K * cap
-  uint32_t* hbo;            // K * cap, hint: lower_bound(hbl) = hbo (relative)
-  uint32_t* hbl;            // K * cap
-  unsigned long long* work;     // cap + 1: (bitmap words << 32 | segments), 0 = not pending
+  unsigned long long* ctr;      // rng counter (key re-derived from the id)
+  double* alpha;                // running scale
+  uint32_t* bnd;                // K * cap
+  uint32_t* hbo;                // K * cap, hint: lower_bound(hbl) = hbo (relative)
+  uint32_t* hbl;                // K * cap
+  unsigned long long* work;     // cap + 1: bitmap words of the pending step, 0 = not pending
   unsigned long long* offsets;  // cap + 1: exclusive scan of work
-  void* desc;               // IsectDesc<K>[cap]
-  uint32_t* bitmap;
+  void* desc;                   // IsectDesc<K>[cap]
+  uint32_t* bitmap;             // fail bits
+  uint32_t* survivors[2];       // compacted survivor lists (double-buffered by step parity)
+  unsigned long long* surv_cursor;  // [2] allocation cursors
+  unsigned long long surv_cap;
   // outputs
   double* values;
   uint32_t* bindings;
@@ -88,18 +91,6 @@ __device__ __forceinline__ uint32_t lb_thread(const uint32_t* base, uint32_t lo,
   return lo;
 }
 
-// branchless lower_bound in base[0, n)
-__device__ __forceinline__ uint32_t lb_branchless(const uint32_t* base, uint32_t n, uint32_t a) {
-  if (n == 0) return 0;
-  uint32_t b = 0;
-  while (n > 1) {
-    const uint32_t half = n >> 1;
-    b = ldn(base, b + half - 1) < a ? b + half : b;
-    n -= half;
-  }
-  return b + (ldn(base, b) < a ? 1u : 0u);
-}
-
 template <int K>
 struct Sample {
   uint32_t bnd[K], hbo[K], hbl[K];
@@ -108,7 +99,17 @@ struct Sample {
   bool loaded[K];
   CounterRng rng;
   double alpha;
-  __device__ Sample(unsigned long long seed, unsigned long long id) : rng(seed, 0, id) {}
+  __device__ Sample(unsigned long long seed, unsigned long long id) : rng(seed, 0, id) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      bnd[q] = INF;
+      hbo[q] = hbl[q] = 0;
+      loaded[q] = false;
+      pb[q] = 0;
+      pd[q] = up[q] = 0;
+    }
+    alpha = 0.0;
+  }
 };
 
 template <int K>
@@ -170,17 +171,12 @@ __device__ void store_state(const FrontierArgs& A, unsigned long long i, const S
 template <int K>
 __device__ void load_state(const FrontierArgs& A, unsigned long long i, Sample<K>& S, int nb) {
 #pragma unroll
-  for (int q = 0; q < K; ++q) {
-    S.loaded[q] = false;
+  for (int q = 0; q < K; ++q)
     if (q < nb) {
       S.bnd[q] = A.bnd[q * A.cap + i];
       S.hbo[q] = A.hbo[q * A.cap + i];
       S.hbl[q] = A.hbl[q * A.cap + i];
-    } else {
-      S.bnd[q] = INF;
-      S.hbo[q] = S.hbl[q] = 0;
     }
-  }
   S.rng.ctr = A.ctr[i];
   S.alpha = A.alpha[i];
 }
@@ -195,33 +191,37 @@ __device__ void finish(const FrontierArgs& A, unsigned long long i, const Sample
   }
 }
 
+// order bounds of step s from the current bindings (walker.hpp:64-69)
 template <int K>
-__device__ __forceinline__ uint32_t dbase_rel(const Sample<K>&, int drv, const uint32_t (&rs)[K]) {
-  uint32_t r = 0;
+__device__ __forceinline__ void step_bounds(const DevPlan& p, int s, const Sample<K>& S, uint32_t& lo, uint32_t& hi) {
+  lo = 0;
+  hi = INF;
 #pragma unroll
-  for (int q = 0; q < K; ++q)
-    if (q == drv) r = rs[q];
-  return r;
+  for (int q = 0; q < K; ++q) {
+    if (q < s + 2 && ((p.gt_mask[s] >> q) & 1u)) lo = max(lo, S.bnd[q] + 1);
+    if (q < s + 2 && ((p.lt_mask[s] >> q) & 1u)) hi = min(hi, S.bnd[q]);
+  }
 }
 
 // Run steps from s0 on: resolve single-list steps inline, stop at the next
-// multi-list step after writing its descriptor, or finish the sample.
+// multi-list step after writing its descriptor, or finish the sample. With
+// `surv` set, step s0 uses those survivors of step s0-1 as its driver and only
+// the lists step s0-1 did not have.
 template <int K>
-__device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& S, int s0) {
+__device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& S, int s0, const uint32_t* surv,
+                        uint32_t surv_len) {
   const uint32_t* __restrict__ nbr = A.g.nbr;
   const DevPlan& p = A.p;
 #pragma unroll
   for (int s = 0; s < K - 2; ++s) {
     if (s < s0) continue;
     const int j = s + 2;
-    const unsigned in_m = p.in_mask[s], out_m = p.out_mask[s];
-    const unsigned gt_m = p.gt_mask[s], lt_m = p.lt_mask[s];
-    uint32_t lo = 0, hi = INF;
-#pragma unroll
-    for (int q = 0; q < j; ++q) {
-      if ((gt_m >> q) & 1u) lo = max(lo, S.bnd[q] + 1);
-      if ((lt_m >> q) & 1u) hi = min(hi, S.bnd[q]);
-    }
+    const bool reuse = s == s0 && surv != nullptr;
+    const unsigned prev_in = reuse && s > 0 ? p.in_mask[s - 1] : 0u;
+    const unsigned prev_out = reuse && s > 0 ? p.out_mask[s - 1] : 0u;
+    const unsigned in_m = p.in_mask[s] & ~prev_in, out_m = p.out_mask[s] & ~prev_out;
+    uint32_t lo, hi;
+    step_bounds(p, s, S, lo, hi);
     uint32_t rs[K], re[K];
     int drv = -1, t_in = 0;
     uint32_t dsize = INF;
@@ -234,16 +234,24 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
         rs[q] = lo ? lbq(nbr, S, q, lo, true) : 0;
         re[q] = hi == INF ? S.pd[q] : lbq(nbr, S, q, hi, false);
         if (re[q] < rs[q]) re[q] = rs[q];
-        if (re[q] - rs[q] < dsize) {
+        if (!reuse && re[q] - rs[q] < dsize) {
           dsize = re[q] - rs[q];
           drv = q;
         }
       }
     }
-    unsigned long long dbase = 0;
+    const uint32_t* dptr = surv;
+    uint32_t drs = 0;
+    if (reuse) {
+      dsize = surv_len;
+    } else {
 #pragma unroll
-    for (int q = 0; q < K; ++q)
-      if (q == drv) dbase = S.pb[q] + rs[q];
+      for (int q = 0; q < K; ++q)
+        if (q == drv) {
+          dptr = nbr + S.pb[q] + rs[q];
+          drs = rs[q];
+        }
+    }
     if (dsize == 0) {
       finish(A, i, S, j, false);
       return;
@@ -256,8 +264,8 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
       for (int q = 0; q < K; ++q) {
         ex[q] = INF;
         if (q < j && S.bnd[q] >= lo && S.bnd[q] < hi) {
-          const uint32_t o = lb_thread(nbr + dbase, 0, dsize, S.bnd[q]);
-          if (o < dsize && ldn(nbr, dbase + o) == S.bnd[q]) {
+          const uint32_t o = lb_thread(dptr, 0, dsize, S.bnd[q]);
+          if (o < dsize && ldn(dptr, o) == S.bnd[q]) {
             ex[q] = o;
             ++nex;
           }
@@ -277,47 +285,38 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
         if (r + c == o) break;
         o = r + c;
       }
-      S.alpha = __dmul_rn(S.alpha, (double)cnt);
-      const uint32_t pick = ldn(nbr, dbase + o);
+      S.alpha = __dmul_rn(S.alpha, (double)cnt);  // alpha *= |S_j| (ns_engine.cpp:39)
+      const uint32_t pick = ldn(dptr, o);
 #pragma unroll
       for (int q = 0; q < j; ++q)
         if (q == drv) {
-          S.hbo[q] = rs[q] + o + 1;
+          S.hbo[q] = drs + o + 1;
           S.hbl[q] = pick + 1;
         }
       bind(S, j, pick);
       continue;
     }
-    // multi-list step: hand the intersection to the merge-path phase
+    // multi-list step: hand the intersection to the word-parallel phase
     IsectDesc<K> d;
-    d.drv = dbase;
+    d.drv = dptr;
     d.dsize = dsize;
-    d.lists = d.outs = d.search = 0;
-    uint32_t segs = 0;
+    d.lists = d.outs = 0;
 #pragma unroll
     for (int q = 0; q < K - 1; ++q) {
       d.start[q] = 0;
       d.len[q] = 0;
-      d.nseg[q] = 0;
       if (q < j && q != drv && (((in_m | out_m) >> q) & 1u)) {
         const bool is_out = (out_m >> q) & 1u;
         d.start[q] = is_out ? S.pb[q] : S.pb[q] + rs[q];
         d.len[q] = is_out ? S.pd[q] : re[q] - rs[q];
         d.lists |= 1u << q;
         if (is_out) d.outs |= 1u << q;
-        if (d.len[q] / kSearchRatio > dsize) {
-          d.search |= 1u << q;
-          d.nseg[q] = (dsize + SEG_SEARCH - 1) / SEG_SEARCH;
-        } else {
-          d.nseg[q] = (dsize + d.len[q] + SEG - 1) / SEG;
-        }
-        segs += d.nseg[q];
       }
     }
-    d.drv_pos = (uint32_t)drv;
-    d.drv_rs = dbase_rel(S, drv, rs);
+    d.drv_pos = reuse ? NO_DRV : (uint32_t)drv;
+    d.drv_rs = drs;
     reinterpret_cast<IsectDesc<K>*>(A.desc)[i] = d;
-    A.work[i] = ((unsigned long long)((dsize + 31) >> 5) << 32) | segs;
+    A.work[i] = (dsize + 31) >> 5;
     store_state(A, i, S, j);
     return;
   }
@@ -329,16 +328,8 @@ __global__ void __launch_bounds__(256) fr_seed_kernel(const FrontierArgs A) {
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < A.count;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     Sample<K> S(A.seed, A.first_id + i);
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-      S.bnd[q] = INF;
-      S.hbo[q] = S.hbl[q] = 0;
-      S.loaded[q] = false;
-      S.pb[q] = 0;
-      S.pd[q] = S.up[q] = 0;
-    }
     S.alpha = A.p.alpha0;
-    const unsigned long long r0 = S.rng.next_below(A.g.arcs);
+    const unsigned long long r0 = S.rng.next_below(A.g.arcs);  // ns_engine.cpp:29-33
     const unsigned long long arc = __ldg(A.g.seed_arcs + r0);
     uint32_t u = (uint32_t)(arc >> 32), v = (uint32_t)arc;
     const bool swapped = A.p.seed_ordered && u > v;
@@ -360,187 +351,223 @@ __global__ void __launch_bounds__(256) fr_seed_kernel(const FrontierArgs A) {
         S.hbl[1] = u + 1;
       }
     }
-    advance<K>(A, i, S, 0);
+    advance<K>(A, i, S, 0, nullptr, 0);
   }
 }
 
-__device__ __forceinline__ void flush_bits(uint32_t* words, uint32_t w, uint32_t bits) {
-  if (bits) atomicOr(words + w, bits);
+// b ascending across lanes (INF padded); does any lane hold a?
+__device__ __forceinline__ bool warp_contains(uint32_t b, uint32_t a) {
+  int pos = 0;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t t = __shfl_sync(FULL, b, pos + s - 1);
+    if (t < a) pos += s;
+  }
+  return __shfl_sync(FULL, b, pos) == a;
 }
 
-// One thread per work item (merge segment or search batch); a warp covers a
-// contiguous run of items, so the owning sample is found by one k-ary search
-// over the scanned offsets and then advanced linearly.
+// One warp per bitmap word; warps walk contiguous word runs so the owning
+// sample is found once (k-ary over the word offsets) and then advanced.
 template <int K>
-__global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, unsigned long long total) {
+__global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, unsigned long long words) {
   const int lane = threadIdx.x & 31;
   const unsigned long long* __restrict__ off = A.offsets;
   const IsectDesc<K>* __restrict__ desc = reinterpret_cast<const IsectDesc<K>*>(A.desc);
   const uint32_t* __restrict__ nbr = A.g.nbr;
+  const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
   const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-  for (unsigned long long base = ((blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5) * 32;
-       base < total; base += nwarps * 32) {
-    // sample of item `base`: last s with seg_off[s] <= base
-    unsigned long long s;
-    {
-      unsigned long long lo = 0, hi = A.count;
-      while (hi - lo > 32) {
-        const unsigned long long step = (hi - lo) / 33;
-        const unsigned long long pos = lo + (unsigned long long)(lane + 1) * step;
-        const unsigned c = __popc(__ballot_sync(FULL, (off[pos] & 0xffffffffull) <= base));
-        const unsigned long long nlo = c ? lo + c * step : lo;
-        hi = c < 32 ? lo + (c + 1) * step : hi;
-        lo = nlo;
-      }
-      const unsigned long long pos = lo + lane;
-      const bool le = pos < hi && (off[pos] & 0xffffffffull) <= base;
-      s = lo + __popc(__ballot_sync(FULL, le)) - 1;
+  const unsigned long long per = (words + nwarps - 1) / nwarps;
+  const unsigned long long w0 = warp * per, w1 = min(words, w0 + per);
+  if (w0 >= w1) return;
+  unsigned long long s;
+  {  // last s with off[s] <= w0
+    unsigned long long lo = 0, hi = A.count;
+    while (hi - lo > 32) {
+      const unsigned long long step = (hi - lo) / 33;
+      const unsigned c = __popc(__ballot_sync(FULL, off[lo + (unsigned long long)(lane + 1) * step] <= w0));
+      const unsigned long long nlo = c ? lo + c * step : lo;
+      hi = c < 32 ? lo + (c + 1) * step : hi;
+      lo = nlo;
     }
-    const unsigned long long g = base + lane;
-    if (g >= total) continue;
-    while ((off[s + 1] & 0xffffffffull) <= g) ++s;
-    const IsectDesc<K>& d = desc[s];  // fields read straight from L1, no local copy
-    uint32_t l = (uint32_t)(g - (off[s] & 0xffffffffull));
-    uint32_t* words = A.bitmap + (off[s] >> 32);
-    const uint32_t* D = nbr + d.drv;
-    const uint32_t nd = d.dsize;
+    const unsigned long long pos = lo + lane;
+    s = lo + __popc(__ballot_sync(FULL, pos < hi && off[pos] <= w0)) - 1;
+  }
+  for (unsigned long long w = w0; w < w1; ++w) {
+    while (off[s + 1] <= w) ++s;  // uniform
+    const IsectDesc<K>& d = desc[s];
+    const uint32_t o = (uint32_t)(w - off[s]) * 32 + lane;
+    const bool valid = o < d.dsize;
+    const uint32_t a = valid ? ldn(d.drv, o) : INF;
+    bool fail = false;
 #pragma unroll
     for (int q = 0; q < K - 1; ++q) {
       if (!((d.lists >> q) & 1u)) continue;
-      if (l >= d.nseg[q]) {
-        l -= d.nseg[q];
-        continue;
-      }
       const uint32_t* B = nbr + d.start[q];
       const uint32_t nb = d.len[q];
-      const bool is_out = (d.outs >> q) & 1u;
-      uint32_t cw = 0xffffffffu, acc = 0;
-      if ((d.search >> q) & 1u) {
-        const uint32_t i0 = l * SEG_SEARCH, i1 = min(nd, i0 + SEG_SEARCH);
-        for (uint32_t i = i0; i < i1; ++i) {
-          const uint32_t x = ldn(D, i);
-          uint32_t lo = 0, hi = nb;
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (ldn(B, mid) < x) lo = mid + 1; else hi = mid;
-          }
-          const bool found = lo < nb && ldn(B, lo) == x;
-          if ((i >> 5) != cw) {
-            if (cw != 0xffffffffu) flush_bits(words, cw, acc);
-            cw = i >> 5;
-            acc = 0;
-          }
-          if (found == is_out) acc |= 1u << (i & 31);
-        }
+      bool found;
+      if (nb <= 32) {
+        found = warp_contains((uint32_t)lane < nb ? ldn(B, lane) : INF, a);
       } else {
-        // merge-path: start of segment l on diagonal dg (D first on ties)
-        const uint32_t dg = l * SEG;
-        uint32_t lo = dg > nb ? dg - nb : 0, hi = min(dg, nd);
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (ldn(D, mid) <= ldn(B, dg - 1 - mid)) lo = mid + 1; else hi = mid;
+        // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then a short per-lane search
+        const uint32_t step = nb / 33u;
+        const uint32_t sp = ldn(B, (uint32_t)(lane + 1) * step);
+        int c = 0;
+#pragma unroll
+        for (int sh = 16; sh >= 1; sh >>= 1) {
+          const uint32_t t = __shfl_sync(FULL, sp, c + sh - 1);
+          if (t < a) c += sh;
         }
-        uint32_t i = lo, jb = dg - lo;
-        const uint32_t steps = min(SEG, nd + nb - dg);
-        uint32_t x = i < nd ? ldn(D, i) : INF;
-        uint32_t y = jb < nb ? ldn(B, jb) : INF;
-        // branchless merge: every lane executes the same instruction stream;
-        // marks go to a 128-bit window starting at i's word (SEG <= 96 bits past it)
-        const uint32_t wbase = i >> 5;
-        unsigned long long m0 = 0, m1 = 0;
-        for (uint32_t t = 0; t < steps; ++t) {
-          const bool take_d = x <= y;  // D first on ties: y = lower_bound(B, x) when D[i] is consumed
-          const bool mark = take_d && ((x == y) == is_out);
-          const uint32_t p = i - (wbase << 5);
-          m0 |= (unsigned long long)(mark && p < 64) << (p & 63);
-          m1 |= (unsigned long long)(mark && p >= 64) << (p & 63);
-          i += take_d;
-          jb += !take_d;
-          const uint32_t k = take_d ? i : jb;
-          const uint32_t lim = take_d ? nd : nb;
-          const uint32_t* src = take_d ? D : B;
-          const uint32_t v = k < lim ? ldn(src, k) : INF;
-          x = take_d ? v : x;
-          y = take_d ? y : v;
-        }
-        flush_bits(words, wbase, (uint32_t)m0);
-        flush_bits(words, wbase + 1, (uint32_t)(m0 >> 32));
-        flush_bits(words, wbase + 2, (uint32_t)m1);
-        flush_bits(words, wbase + 3, (uint32_t)(m1 >> 32));
-        break;
+        c += __shfl_sync(FULL, sp, c) < a ? 1 : 0;  // c = #splitters < a, in [0, 32]
+        const uint32_t lo = c ? (uint32_t)c * step + 1 : 0;
+        const uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step : nb;
+        const uint32_t at = lb_thread(B, lo, hi, a);
+        found = at < nb && ldn(B, at) == a;
       }
-      if (cw != 0xffffffffu) flush_bits(words, cw, acc);
-      break;
+      fail = fail || (found == (bool)((d.outs >> q) & 1u));
+    }
+    const unsigned bal = __ballot_sync(FULL, valid && fail);
+    if (lane == 0) A.bitmap[w] = bal;
+  }
+}
+
+// Thread per sample, warp-uniform loop structure so survivor compaction can use
+// one atomic per warp.
+template <int K>
+__global__ void __launch_bounds__(256) fr_pick_kernel(const FrontierArgs A, int s_step) {
+  const uint32_t* __restrict__ nbr = A.g.nbr;
+  const int lane = threadIdx.x & 31;
+  const int j = s_step + 2;
+  const bool reuse_next = s_step + 1 < K - 2 && A.step_reuse[s_step + 1];
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long base = (blockIdx.x * (unsigned long long)blockDim.x) + (threadIdx.x & ~31u);
+       base < A.count; base += stride) {
+    const unsigned long long i = base + lane;
+    const bool act = i < A.count && A.work[i] != 0;
+    Sample<K> S(A.seed, A.first_id + (act ? i : 0));
+    bool alive = false;
+    uint32_t o_pick = 0, nsurv = 0, lo2 = 0, hi2 = INF, pick = 0;
+    const IsectDesc<K>* dp = reinterpret_cast<const IsectDesc<K>*>(A.desc) + (act ? i : 0);
+    const uint32_t* words = A.bitmap + (act ? A.offsets[i] : 0);
+    uint32_t ex[K];
+    uint32_t dsize = 0;
+    if (act) {
+      load_state(A, i, S, j);
+      dsize = dp->dsize;
+      const uint32_t* D = dp->drv;
+      uint32_t lo, hi;
+      step_bounds(A.p, s_step, S, lo, hi);
+      // bound vertices that survived the intersection are not candidates (walker.hpp:70-82)
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        ex[q] = INF;
+        if (q < j && S.bnd[q] >= lo && S.bnd[q] < hi) {
+          const uint32_t o = lb_thread(D, 0, dsize, S.bnd[q]);
+          if (o < dsize && ldn(D, o) == S.bnd[q] && !((words[o >> 5] >> (o & 31)) & 1u)) ex[q] = o;
+        }
+      }
+      const uint32_t nw = (dsize + 31) >> 5;
+      auto live = [&](uint32_t w) -> unsigned {
+        unsigned m = ~words[w];
+        if (w == nw - 1 && (dsize & 31)) m &= (1u << (dsize & 31)) - 1u;
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+          if (ex[q] != INF && (ex[q] >> 5) == w) m &= ~(1u << (ex[q] & 31));
+        return m;
+      };
+      unsigned long long cnt = 0;
+      for (uint32_t w = 0; w < nw; ++w) cnt += __popc(live(w));
+      if (cnt == 0) {
+        finish(A, i, S, j, false);
+      } else {
+        unsigned long long r = S.rng.next_below(cnt);
+        for (uint32_t w = 0; w < nw; ++w) {
+          const unsigned m = live(w);
+          const unsigned pc = __popc(m);
+          if (r < pc) {
+            o_pick = w * 32 + __fns(m, 0, (int)r + 1);
+            break;
+          }
+          r -= pc;
+        }
+        S.alpha = __dmul_rn(S.alpha, (double)cnt);  // alpha *= |S_j| (ns_engine.cpp:39)
+        pick = ldn(D, o_pick);
+        if (dp->drv_pos != NO_DRV) {
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if ((uint32_t)q == dp->drv_pos) {  // lower_bound(pick + 1) = drv_rs + o + 1
+              S.hbo[q] = dp->drv_rs + o_pick + 1;
+              S.hbl[q] = pick + 1;
+            }
+        }
+        bind(S, j, pick);
+        alive = true;
+        if (reuse_next) {
+          step_bounds(A.p, s_step + 1, S, lo2, hi2);
+          for (uint32_t w = 0; w < nw; ++w) {
+            unsigned m = live(w);
+            while (m) {
+              const uint32_t o = w * 32 + __ffs(m) - 1;
+              m &= m - 1;
+              const uint32_t x = ldn(D, o);
+              nsurv += (o != o_pick && x >= lo2 && x < hi2) ? 1u : 0u;
+            }
+          }
+        }
+      }
+    }
+    // warp-aggregated allocation of the survivor lists
+    uint32_t* surv = nullptr;
+    if (reuse_next) {
+      unsigned incl = nsurv;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned t = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += t;
+      }
+      unsigned long long wbase = 0;
+      if (lane == 31 && incl) wbase = atomicAdd(A.surv_cursor + ((s_step + 1) & 1), (unsigned long long)incl);
+      wbase = __shfl_sync(FULL, wbase, 31);
+      const unsigned long long at = wbase + incl - nsurv;
+      surv = A.survivors[(s_step + 1) & 1] + (at < A.surv_cap ? at : 0);
+      if (alive && nsurv && at + nsurv <= A.surv_cap) {
+        const uint32_t nw = (dsize + 31) >> 5;
+        uint32_t k = 0;
+        for (uint32_t w = 0; w < nw; ++w) {
+          unsigned m = ~words[w];
+          if (w == nw - 1 && (dsize & 31)) m &= (1u << (dsize & 31)) - 1u;
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if (ex[q] != INF && (ex[q] >> 5) == w) m &= ~(1u << (ex[q] & 31));
+          while (m) {
+            const uint32_t o = w * 32 + __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t x = ldn(dp->drv, o);
+            if (o != o_pick && x >= lo2 && x < hi2) surv[k++] = x;
+          }
+        }
+      }
+    }
+    if (alive) {
+      if (reuse_next)
+        advance<K>(A, i, S, s_step + 1, surv, nsurv);
+      else
+        advance<K>(A, i, S, s_step + 1, nullptr, 0);
     }
   }
 }
 
-template <int K>
-__global__ void __launch_bounds__(256) fr_pick_kernel(const FrontierArgs A, int s_step) {
-  const uint32_t* __restrict__ nbr = A.g.nbr;
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < A.count;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    if (A.work[i] == 0) continue;
-    const int j = s_step + 2;
-    Sample<K> S(A.seed, A.first_id + i);
-    load_state(A, i, S, j);
-    const IsectDesc<K> d = reinterpret_cast<const IsectDesc<K>*>(A.desc)[i];
-    const uint32_t dsize = d.dsize;
-    const uint32_t* words = A.bitmap + (A.offsets[i] >> 32);
-    uint32_t lo = 0, hi = INF;
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-      if (q < j && ((A.p.gt_mask[s_step] >> q) & 1u)) lo = max(lo, S.bnd[q] + 1);
-      if (q < j && ((A.p.lt_mask[s_step] >> q) & 1u)) hi = min(hi, S.bnd[q]);
-    }
-    // bound vertices that survived the intersection are not candidates (walker.hpp:70-82)
-    uint32_t ex[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-      ex[q] = INF;
-      if (q < j && S.bnd[q] >= lo && S.bnd[q] < hi) {
-        const uint32_t o = lb_thread(nbr + d.drv, 0, dsize, S.bnd[q]);
-        if (o < dsize && ldn(nbr, d.drv + o) == S.bnd[q] && !((words[o >> 5] >> (o & 31)) & 1u)) ex[q] = o;
-      }
-    }
-    const uint32_t nw = (dsize + 31) >> 5;
-    auto live = [&](uint32_t w) -> unsigned {  // surviving candidates in word w
-      unsigned m = ~words[w];
-      if (w == nw - 1 && (dsize & 31)) m &= (1u << (dsize & 31)) - 1u;
-#pragma unroll
-      for (int q = 0; q < K; ++q)
-        if (ex[q] != INF && (ex[q] >> 5) == w) m &= ~(1u << (ex[q] & 31));
-      return m;
-    };
-    unsigned long long cnt = 0;
-    for (uint32_t w = 0; w < nw; ++w) cnt += __popc(live(w));
-    if (cnt == 0) {
-      finish(A, i, S, j, false);
-      continue;
-    }
-    unsigned long long r = S.rng.next_below(cnt);
-    uint32_t o = 0;
-    for (uint32_t w = 0; w < nw; ++w) {
-      const unsigned m = live(w);
-      const unsigned pc = __popc(m);
-      if (r < pc) {
-        o = w * 32 + __fns(m, 0, (int)r + 1);
-        break;
-      }
-      r -= pc;
-    }
-    S.alpha = __dmul_rn(S.alpha, (double)cnt);  // alpha *= |S_j| (ns_engine.cpp:39)
-    const uint32_t pick = ldn(nbr, d.drv + o);
-    // the pick sits at drv_rs + o in the driver's list: lower_bound(pick+1) = drv_rs + o + 1
-#pragma unroll
-    for (int q = 0; q < K; ++q)
-      if ((uint32_t)q == d.drv_pos) {
-        S.hbo[q] = d.drv_rs + o + 1;
-        S.hbl[q] = pick + 1;
-      }
-    bind(S, j, pick);
-    advance<K>(A, i, S, s_step + 1);
-  }
+// step s can reuse step s-1's survivors when its lists and bounds nest
+bool nests(const DevPlan& p, int s) {
+  if (s == 0) return false;
+  const unsigned pin = p.in_mask[s - 1], pout = p.out_mask[s - 1], in = p.in_mask[s], out = p.out_mask[s];
+  if ((pin & in) != pin || (pout & out) != pout) return false;
+  if (__builtin_popcount(pin) == 1 && pout == 0) return false;  // previous step was single-list
+  const unsigned prev_pos = 1u << (s + 1);                         // position bound by step s-1
+  const bool lo_ok = p.gt_mask[s - 1] == 0 || (p.gt_mask[s] & prev_pos) ||
+                     (p.gt_mask[s] & p.gt_mask[s - 1]) == p.gt_mask[s - 1];
+  const bool hi_ok = p.lt_mask[s - 1] == 0 || (p.lt_mask[s] & prev_pos) ||
+                     (p.lt_mask[s] & p.lt_mask[s - 1]) == p.lt_mask[s - 1];
+  return lo_ok && hi_ok;
 }
 
 template <int K>
@@ -553,6 +580,7 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
   for (int st = 0; st < K - 2; ++st) {
     const unsigned in_m = L.p.in_mask[st], out_m = L.p.out_mask[st];
     A.step_multi[st] = !(__builtin_popcount(in_m) == 1 && out_m == 0);
+    A.step_reuse[st] = A.step_multi[st] && nests(L.p, st);
   }
   const unsigned long long cap = std::min<unsigned long long>(L.count, 1ull << 22);
   A.cap = cap;
@@ -564,7 +592,7 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
   };
   const size_t o_ctr = carve(8 * cap), o_alpha = carve(8 * cap), o_bnd = carve(4ull * K * cap),
                o_hbo = carve(4ull * K * cap), o_hbl = carve(4ull * K * cap), o_work = carve(8 * (cap + 1)),
-               o_off = carve(8 * (cap + 1)), o_desc = carve(sizeof(IsectDesc<K>) * cap);
+               o_off = carve(8 * (cap + 1)), o_desc = carve(sizeof(IsectDesc<K>) * cap), o_cur = carve(64);
   size_t scan_tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (const unsigned long long*)nullptr,
                                 (unsigned long long*)nullptr, (int64_t)cap + 1, s);
@@ -578,8 +606,11 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
   A.work = reinterpret_cast<unsigned long long*>(slab + o_work);
   A.offsets = reinterpret_cast<unsigned long long*>(slab + o_off);
   A.desc = slab + o_desc;
+  A.surv_cursor = reinterpret_cast<unsigned long long*>(slab + o_cur);
   void* tmp = slab + o_tmp;
   auto* h_total = static_cast<unsigned long long*>(ctx.get_pinned(2, 64));
+  bool any_reuse = false;
+  for (int st = 0; st < K - 2; ++st) any_reuse = any_reuse || A.step_reuse[st];
 
   const int sms = ctx.sm_count;
   for (unsigned long long done = 0; done < L.count; done += cap) {
@@ -599,12 +630,17 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
       AGPM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, A.work, A.offsets, (int64_t)c + 1, s));
       AGPM_CUDA(cudaMemcpyAsync(h_total, A.offsets + c, 8, cudaMemcpyDeviceToHost, s));
       AGPM_CUDA(cudaStreamSynchronize(s));
-      const unsigned long long words = *h_total >> 32, segs = *h_total & 0xffffffffull;
+      const unsigned long long words = *h_total;
       if (words) {
         A.bitmap = static_cast<uint32_t*>(ctx.get(8, 4 * words + 64));
-        AGPM_CUDA(cudaMemsetAsync(A.bitmap, 0, 4 * words, s));
-        const unsigned long long warps = std::min<unsigned long long>((segs + 31) / 32, (unsigned long long)sms * 64);
-        fr_isect_kernel<K><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(A, segs);
+        if (any_reuse) {  // survivors <= driver elements <= 32 * words
+          A.surv_cap = 32 * words;
+          const int slot = (st + 1) & 1;
+          A.survivors[slot] = static_cast<uint32_t*>(ctx.get(10 + slot, 4 * A.surv_cap + 64));
+          AGPM_CUDA(cudaMemsetAsync(A.surv_cursor + slot, 0, 8, s));
+        }
+        const unsigned long long warps = std::min<unsigned long long>(words, (unsigned long long)sms * 64);
+        fr_isect_kernel<K><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(A, words);
         count_launch();
         AGPM_CUDA(cudaGetLastError());
       }
@@ -619,8 +655,8 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
 
 void launch_ns_frontier(const SampleLaunch& L, cudaStream_t s) {
   if (L.bytes_out) throw std::invalid_argument("B_min accounting runs on the warp sampler");
-#define AGPM_K(KK)          \
-  case KK:                  \
+#define AGPM_K(KK)            \
+  case KK:                    \
     run_frontier_k<KK>(L, s); \
     break;
   switch (L.p.k) {
