@@ -193,6 +193,9 @@ int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delt
  * (tiny adjacency lists), 3 = frontier phases (element-parallel
  * intersections over a whole batch). All strategies draw identical samples. */
 int agpm_ns_set_strategy(int strategy);
+/* frontier only: let a step whose lists nest the previous step's (cliques)
+ * intersect that step's survivors instead of recomputing (same samples). */
+int agpm_ns_set_frontier_reuse(int on);
 
 /* Device-pointer building blocks (bench / multi-rank driver): enqueue only.
  * d_values: count f64 device buffer. */

@@ -119,6 +119,7 @@ def _declare(L):
         "agpm_window_moments_dev": (C.c_int, [A.P, A.u64, A.u64, A.P, A.P]),
         "agpm_ns_bmin_bytes": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pu64, A.P]),
         "agpm_ns_set_strategy": (C.c_int, [C.c_int]),
+        "agpm_ns_set_frontier_reuse": (C.c_int, [C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -380,6 +381,11 @@ STRATEGIES = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3}
 def set_strategy(name):
     """Sampler kernel choice (all draw identical samples): auto | warp | lane | frontier."""
     _check(lib().agpm_ns_set_strategy(STRATEGIES[name]))
+
+
+def set_frontier_reuse(on):
+    """Frontier sampler: reuse nested survivors between clique steps (same samples)."""
+    _check(lib().agpm_ns_set_frontier_reuse(int(bool(on))))
 
 
 def kernel_launches():

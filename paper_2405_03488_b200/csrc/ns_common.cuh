@@ -79,5 +79,6 @@ __device__ __forceinline__ unsigned long long sectors(unsigned long long a, unsi
 void launch_ns_lane(const SampleLaunch& L, cudaStream_t s);
 void launch_ns_warp(const SampleLaunch& L, cudaStream_t s);
 void launch_ns_frontier(const SampleLaunch& L, cudaStream_t s);
+void set_frontier_reuse(bool on);
 
 }  // namespace agpm_b200

@@ -204,6 +204,10 @@ int agpm_ns_set_strategy(int strategy) {
   });
 }
 
+int agpm_ns_set_frontier_reuse(int on) {
+  return guarded([&] { set_frontier_reuse(on != 0); });
+}
+
 int agpm_ns_sample_dev(agpm_graph* g, const agpm_plan* plan, uint64_t seed, uint64_t first_id,
                        uint64_t count, double* d_values, void* stream) {
   return guarded([&] {

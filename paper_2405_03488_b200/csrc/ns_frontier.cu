@@ -556,6 +556,11 @@ __global__ void __launch_bounds__(256) fr_pick_kernel(const FrontierArgs A, int 
   }
 }
 
+// Nested survivor reuse is exact but, at word granularity, rarely cheaper than
+// re-intersecting (a sample's step-j driver is ~1 bitmap word either way) while
+// compaction makes the pick phase divergent; off unless enabled.
+bool g_frontier_reuse = false;
+
 // step s can reuse step s-1's survivors when its lists and bounds nest
 bool nests(const DevPlan& p, int s) {
   if (s == 0) return false;
@@ -580,7 +585,7 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
   for (int st = 0; st < K - 2; ++st) {
     const unsigned in_m = L.p.in_mask[st], out_m = L.p.out_mask[st];
     A.step_multi[st] = !(__builtin_popcount(in_m) == 1 && out_m == 0);
-    A.step_reuse[st] = A.step_multi[st] && nests(L.p, st);
+    A.step_reuse[st] = g_frontier_reuse && A.step_multi[st] && nests(L.p, st);
   }
   const unsigned long long cap = std::min<unsigned long long>(L.count, 1ull << 22);
   A.cap = cap;
@@ -652,6 +657,8 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
 }
 
 }  // namespace
+
+void set_frontier_reuse(bool on) { g_frontier_reuse = on; }
 
 void launch_ns_frontier(const SampleLaunch& L, cudaStream_t s) {
   if (L.bytes_out) throw std::invalid_argument("B_min accounting runs on the warp sampler");

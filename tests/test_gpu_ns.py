@@ -36,11 +36,13 @@ def graphs(agpm):
     return _graphs(agpm)
 
 
-@pytest.fixture(params=["warp", "lane", "frontier"])
+@pytest.fixture(params=["warp", "lane", "frontier", "frontier_reuse"])
 def strategy(agpm, request):
-    agpm.set_strategy(request.param)
+    agpm.set_strategy(request.param.split("_")[0])
+    agpm.set_frontier_reuse(request.param == "frontier_reuse")
     yield request.param
     agpm.set_strategy("auto")
+    agpm.set_frontier_reuse(False)
 
 
 @pytest.mark.parametrize("name", ["er200", "er200_rel", "er60_dense", "rmat12_rel", "rmat12"])
