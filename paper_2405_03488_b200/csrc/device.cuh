@@ -61,6 +61,8 @@ struct agpm_graph {
   agpm_b200::VtxInfo* vtx = nullptr;
   uint32_t* nbr = nullptr;
   unsigned long long* seed_arcs = nullptr;
+  unsigned long long* ehash = nullptr;  // edge-membership table (edge_hash.cuh), built on demand
+  uint32_t ehash_mask = 0;
   uint64_t bytes = 0;
 };
 
@@ -70,4 +72,6 @@ namespace agpm_b200 {
 // ownership of nothing; g->nbr must be set.
 void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsigned long long* d_end,
                    cudaStream_t s);
+// build g->ehash if absent (symmetric or oriented views alike: keys are unordered pairs)
+void ensure_edge_hash(agpm_graph* g, cudaStream_t s);
 }  // namespace agpm_b200

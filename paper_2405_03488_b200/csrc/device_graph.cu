@@ -226,6 +226,7 @@ int agpm_graph_free(agpm_graph* g) {
     cudaFree(g->vtx);
     cudaFree(g->nbr);
     cudaFree(g->seed_arcs);
+    if (g->ehash) cudaFree(g->ehash);
     delete g;
   });
 }

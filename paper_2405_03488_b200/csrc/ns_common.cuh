@@ -35,6 +35,8 @@ struct GraphArgs {
   const unsigned long long* __restrict__ seed_arcs;
   unsigned long long arcs;
   int plain;
+  const unsigned long long* __restrict__ ehash;  // edge table (frontier sampler)
+  uint32_t ehash_mask;
 };
 
 struct SampleLaunch {

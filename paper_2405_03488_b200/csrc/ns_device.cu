@@ -142,6 +142,8 @@ GraphArgs graph_args(const agpm_graph* g) {
   a.seed_arcs = g->seed_arcs;
   a.arcs = g->arcs;
   a.plain = g->plain;
+  a.ehash = g->ehash;
+  a.ehash_mask = g->ehash_mask;
   return a;
 }
 
@@ -164,9 +166,10 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
   DeviceCtx& ctx = ctx_for_current_device();
   auto* cursor = static_cast<unsigned long long*>(ctx.get(0, 64));
   AGPM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
-  SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};
   if (dp.k < 3 || dp.k > AGPM_MAX_K) throw std::invalid_argument("device sampler needs 3 <= k <= 9");
   const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, count);  // B_min replay: warp kernel
+  if (strat == kStrategyFrontier) ensure_edge_hash(const_cast<agpm_graph*>(g), s);
+  SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};
   if (strat == kStrategyLane)
     launch_ns_lane(L, s);
   else if (strat == kStrategyFrontier)

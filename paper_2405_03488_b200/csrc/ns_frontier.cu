@@ -10,11 +10,12 @@
 //   scan     (CUB)                  word offsets: every sample's hit bitmap
 //            starts on a 32-bit word boundary.
 //   isect    (1 warp / bitmap word) a word = 32 driver elements of ONE sample.
-//            Per other list the warp loads 32 splitters in one coalesced load,
-//            each lane finds its bucket with a 5-step shuffle search and
-//            finishes with a ~3-level per-lane search (lists <= 32 elements:
-//            one load + shuffle membership). One ballot -> the fail word. No
-//            atomics, no memset, every lane busy whatever the skew.
+//            Every "a in list q" test is one probe of the device edge table
+//            (edge_hash.cuh: one 32-B bucket per lookup), since the driver
+//            already sits inside the step's [lo, hi). Without a table the warp
+//            loads 32 splitters of list q, finds each lane's bucket with a
+//            5-step shuffle search and finishes with a short per-lane search.
+//            One ballot -> the fail word. No atomics, no memset.
 //   pick     (1 thread / sample)    |S_j| = |D| - fails - bound vertices,
 //            r = next_below(|S_j|), r-th surviving bit -> v_j, alpha *= |S_j|.
 //            Nested reuse: when step j+1's lists contain step j's (cliques),
@@ -33,6 +34,7 @@
 #include <algorithm>
 #include <stdexcept>
 
+#include "edge_hash.cuh"
 #include "ns_common.cuh"
 
 namespace agpm_b200 {
@@ -48,6 +50,7 @@ struct __align__(16) IsectDesc {
   const uint32_t* drv;                // driver list (adjacency range or compacted survivors)
   unsigned long long start[K - 1];    // other lists: in-lists restricted, out-lists whole
   uint32_t len[K - 1];
+  uint32_t owner[K - 1];              // bound vertex whose adjacency list slot q is
   uint32_t dsize;
   uint32_t lists;                     // bit q: position q is an other list
   uint32_t outs;                      // bit q: ... and an out-list (difference)
@@ -305,6 +308,7 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
     for (int q = 0; q < K - 1; ++q) {
       d.start[q] = 0;
       d.len[q] = 0;
+      d.owner[q] = S.bnd[q];
       if (q < j && q != drv && (((in_m | out_m) >> q) & 1u)) {
         const bool is_out = (out_m >> q) & 1u;
         d.start[q] = is_out ? S.pb[q] : S.pb[q] + rs[q];
@@ -402,10 +406,13 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
 #pragma unroll
     for (int q = 0; q < K - 1; ++q) {
       if (!((d.lists >> q) & 1u)) continue;
+      bool found;
       const uint32_t* B = nbr + d.start[q];
       const uint32_t nb = d.len[q];
-      bool found;
-      if (nb <= 32) {
+      if (A.g.ehash) {
+        // a is inside [lo, hi) already, so membership in the restricted list is edge existence
+        found = valid && edge_lookup(A.g.ehash, A.g.ehash_mask, a, d.owner[q]);
+      } else if (nb <= 32) {
         found = warp_contains((uint32_t)lane < nb ? ldn(B, lane) : INF, a);
       } else {
         // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then a short per-lane search
