@@ -142,8 +142,8 @@ GraphArgs graph_args(const agpm_graph* g) {
   a.seed_arcs = g->seed_arcs;
   a.arcs = g->arcs;
   a.plain = g->plain;
-  a.ehash = g->ehash;
-  a.ehash_mask = g->ehash_mask;
+  a.ehash = nullptr;  // see enqueue_sample
+  a.ehash_mask = 0;
   return a;
 }
 
@@ -168,7 +168,8 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
   AGPM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
   if (dp.k < 3 || dp.k > AGPM_MAX_K) throw std::invalid_argument("device sampler needs 3 <= k <= 9");
   const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, count);  // B_min replay: warp kernel
-  if (strat == kStrategyFrontier) ensure_edge_hash(const_cast<agpm_graph*>(g), s);
+  // (the edge-hash membership path is available but off: on RMAT-20 it turned
+  // L2-local list searches into random HBM sectors and ran 2.6x slower)
   SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};
   if (strat == kStrategyLane)
     launch_ns_lane(L, s);
