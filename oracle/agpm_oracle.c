@@ -289,8 +289,8 @@ static void build_step_candidates(const view_t* g, const agpm_plan* plan, int si
   if (plan->verify_mode == 0) {
     /* lists sorted by size, stable like std::sort on (size) — set result is
        order-independent, so any tie order gives the same candidate set */
-    const uint32_t* lp[AGPM_MAX_K];
-    size_t ln[AGPM_MAX_K];
+    const uint32_t* lp[AGPM_MAX_K] = {0};
+    size_t ln[AGPM_MAX_K] = {0};
     int nl = st->n_in;
     for (int i = 0; i < nl; ++i) {
       uint32_t b = binding[st->in_positions[i]];
