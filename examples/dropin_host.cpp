@@ -1,0 +1,38 @@
+// Reference-style caller compiled against the drop-in header (include/agpm/agpm.hpp)
+// and linked with libagpm_b200.so. Host-only parts run anywhere; the sampling
+// calls need a B200 (they throw agpm::device_error otherwise — no CPU fallback).
+#include <cstdio>
+#include <string>
+
+#include "agpm/agpm.hpp"
+
+int main(int argc, char** argv) {
+  const bool device = argc > 1 && std::string(argv[1]) == "--device";
+  agpm::ExecutionPlan plan = agpm::compile_plan(agpm::parse_pattern_spec("4clique"), agpm::VerifyMode::Eager);
+  std::printf("plan %s k=%d steps=%zu seed_ordered=%d rule='%s'\n", plan.pattern.name.c_str(), plan.k(),
+              plan.steps.size(), (int)plan.seed_ordered, plan.scaling_rule_text().c_str());
+  agpm::Pattern hand;
+  hand.vertex_count = 4;
+  hand.edges = {{0, 1}, {1, 2}, {2, 3}, {3, 0}};
+  std::printf("hand-built 4-cycle rule='%s'\n", agpm::compile_plan(hand, agpm::VerifyMode::Eager).scaling_rule_text().c_str());
+  try {
+    agpm::parse_pattern_spec("pentagon");
+  } catch (const agpm::pattern_error& e) {
+    std::printf("pattern_error ok\n");
+  }
+  agpm::CsrGraph g = agpm::CsrGraph::from_edges({{0, 1}, {1, 2}, {0, 2}, {2, 3}, {1, 3}, {0, 3}});
+  std::printf("graph n=%u m=%llu\n", g.vertex_count(), (unsigned long long)g.edge_count());
+  agpm::SampleAccumulator acc;
+  acc.add(0.0, false);
+  acc.add(4.0, true);
+  std::printf("eps_hat=%.5f\n", agpm::predicted_error(acc, 0.05).epsilon_hat);
+  if (device) {
+    agpm::OnlineResult r = agpm::run_ns_online(g.view(), plan, 0.05, 0.05, agpm::OnlinePolicy{}, 7);
+    std::printf("K4 4-cliques ~ %.4f (n=%llu converged=%d)\n", r.report.mu, (unsigned long long)r.report.n,
+                (int)r.report.converged);
+    agpm::CounterRng rng(7, 0, 3);
+    agpm::SampledCount s = agpm::draw_sample(g.view(), plan, rng);
+    std::printf("draw value=%.1f hit=%d\n", s.value, (int)s.hit);
+  }
+  return 0;
+}

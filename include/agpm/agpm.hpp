@@ -1,0 +1,424 @@
+// agpm/agpm.hpp — header-only C++ drop-in for the reference's sampling API.
+//
+// Same namespace, type names and call shapes as the reference library
+// (/root/reference/proj/include/agpm/*.hpp) for the hot path, implemented
+// inline over the C ABI of libagpm_b200.so (include/agpm_b200.h). A caller of
+//   agpm::run_ns_online(g.view(), agpm::compile_plan(p, agpm::VerifyMode::Eager),
+//                       eps, delta, agpm::OnlinePolicy{}, seed)
+// relinks against libagpm_b200 and runs on the B200 unchanged. Error
+// behaviour mirrors the reference: std::invalid_argument, agpm::pattern_error,
+// agpm::io_error, agpm::parse_error (+ agpm::device_error for CUDA faults).
+//
+// Device mirrors of a CsrView are cached by the view's pointers: the
+// reference documents CsrGraph / CsrView as immutable (csr_graph.hpp:19-22,
+// 43-45), so pointer identity identifies the data.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <list>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include "agpm_b200.h"
+
+namespace agpm {
+
+struct parse_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct io_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct pattern_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct device_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void check(int status) {
+  if (status == AGPM_OK) return;
+  const std::string msg = agpm_last_error();
+  switch (status) {
+    case AGPM_E_INVALID: throw std::invalid_argument(msg);
+    case AGPM_E_PATTERN: throw pattern_error(msg);
+    case AGPM_E_IO: throw io_error(msg);
+    case AGPM_E_PARSE: throw parse_error(msg);
+    default: throw device_error(msg);
+  }
+}
+}  // namespace detail
+
+// ------------------------------------------------------------------ rng.hpp
+// Host CounterRng with the reference's exact stream (rng.hpp:26-56).
+inline uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
+}
+inline uint64_t derive_key(uint64_t seed, uint64_t s1 = 0, uint64_t s2 = 0) {
+  uint64_t h = mix64(seed + 0x9e3779b97f4a7c15ull);
+  h = mix64(h ^ (s1 + 0xbf58476d1ce4e5b9ull));
+  return mix64(h ^ (s2 + 0x94d049bb133111ebull));
+}
+class CounterRng {
+ public:
+  explicit CounterRng(uint64_t seed, uint64_t stream1 = 0, uint64_t stream2 = 0)
+      : seed_(seed), s1_(stream1), s2_(stream2), key_(derive_key(seed, stream1, stream2)) {}
+  uint64_t next_u64() {
+    ctr_ += 0x9e3779b97f4a7c15ull;
+    return mix64(key_ ^ ctr_);
+  }
+  double next_double() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+  uint64_t next_below(uint64_t n) {
+    unsigned __int128 m = static_cast<unsigned __int128>(next_u64()) * n;
+    auto lo = static_cast<uint64_t>(m);
+    if (lo < n) {
+      uint64_t t = (0 - n) % n;
+      while (lo < t) {
+        m = static_cast<unsigned __int128>(next_u64()) * n;
+        lo = static_cast<uint64_t>(m);
+      }
+    }
+    return static_cast<uint64_t>(m >> 64);
+  }
+  // stream identity (device draws regenerate the stream from it)
+  uint64_t seed() const { return seed_; }
+  uint64_t stream1() const { return s1_; }
+  uint64_t stream2() const { return s2_; }
+  bool fresh() const { return ctr_ == 0; }
+
+ private:
+  uint64_t seed_, s1_, s2_, key_;
+  uint64_t ctr_ = 0;
+};
+
+// ------------------------------------------------------------------ stats.hpp
+struct SampleAccumulator {
+  uint64_t n = 0;
+  uint64_t hits = 0;
+  double sum = 0.0;
+  double squared_sum = 0.0;
+  void add(double value, bool hit) {
+    ++n;
+    if (hit) ++hits;
+    sum += value;
+    squared_sum += value * value;
+  }
+  void merge(const SampleAccumulator& o) {
+    n += o.n;
+    hits += o.hits;
+    sum += o.sum;
+    squared_sum += o.squared_sum;
+  }
+};
+
+struct ConvergenceReport {
+  double mu = 0.0;
+  double sigma = 0.0;
+  double epsilon_hat = 0.0;
+  uint64_t n = 0;
+  bool converged = false;
+  double hit_rate = 0.0;
+};
+
+inline double norm_cdf(double z) { return agpm_norm_cdf(z); }
+inline double inv_norm_cdf(double q) {
+  double out = 0;
+  detail::check(agpm_inv_norm_cdf(q, &out));
+  return out;
+}
+namespace detail {
+inline ConvergenceReport from_c(const agpm_report& r) {
+  return {r.mu, r.sigma, r.epsilon_hat, r.n, r.converged != 0, r.hit_rate};
+}
+inline SampleAccumulator from_c(const agpm_accumulator& a) { return {a.n, a.hits, a.sum, a.squared_sum}; }
+}  // namespace detail
+inline ConvergenceReport predicted_error(const SampleAccumulator& acc, double delta) {
+  agpm_accumulator a{acc.n, acc.hits, acc.sum, acc.squared_sum};
+  agpm_report r{};
+  detail::check(agpm_predicted_error(&a, delta, &r));
+  return detail::from_c(r);
+}
+
+// ------------------------------------------------------------------ pattern.hpp / plan.hpp
+enum class InducedMode { Edge, Vertex };
+enum class VerifyMode { Eager, Lazy };
+
+struct Pattern {
+  std::string name;
+  int vertex_count = 0;
+  std::vector<std::pair<int, int>> edges;
+  InducedMode induced = InducedMode::Edge;
+  std::string spec;  // how the ABI rebuilds it
+  int edge_count() const { return static_cast<int>(edges.size()); }
+  bool is_clique() const { return edge_count() == vertex_count * (vertex_count - 1) / 2; }
+};
+
+struct PlanStep {
+  int pattern_vertex = -1;
+  std::vector<int> in_positions, out_positions, greater_than, less_than;
+  int tree_parent = -1;
+  std::vector<std::pair<int, int>> verify_edges;
+};
+
+struct ExecutionPlan {
+  Pattern pattern;
+  VerifyMode verify_mode = VerifyMode::Eager;
+  std::vector<int> order, pos_of;
+  bool seed_ordered = false;
+  bool symmetry_enabled = true;
+  std::vector<PlanStep> steps;
+  std::vector<std::pair<int, int>> closure_edges, constraints, terminal_constraints;
+  agpm_plan c{};  // the ABI image
+  int k() const { return pattern.vertex_count; }
+  bool is_clique() const { return pattern.is_clique(); }
+  double seed_scale(uint64_t edge_count) const {
+    return seed_ordered ? static_cast<double>(edge_count) : 2.0 * static_cast<double>(edge_count);
+  }
+  std::string scaling_rule_text() const {
+    char buf[512];
+    detail::check(agpm_plan_scaling_rule(&c, buf, sizeof(buf)));
+    return buf;
+  }
+};
+
+namespace detail {
+inline std::vector<std::pair<int, int>> pairs(int n, const int32_t (*a)[2]) {
+  std::vector<std::pair<int, int>> v;
+  for (int i = 0; i < n; ++i) v.emplace_back(a[i][0], a[i][1]);
+  return v;
+}
+inline ExecutionPlan from_c(const agpm_plan& c, const std::string& spec) {
+  ExecutionPlan p;
+  p.c = c;
+  p.pattern.name = c.name;
+  p.pattern.vertex_count = c.k;
+  p.pattern.edges = pairs(c.n_edges, c.edges);
+  p.pattern.induced = c.induced ? InducedMode::Vertex : InducedMode::Edge;
+  p.pattern.spec = spec;
+  p.verify_mode = c.verify_mode ? VerifyMode::Lazy : VerifyMode::Eager;
+  p.order.assign(c.order, c.order + c.k);
+  p.pos_of.assign(c.pos_of, c.pos_of + c.k);
+  p.seed_ordered = c.seed_ordered;
+  p.symmetry_enabled = c.symmetry_enabled;
+  for (int s = 0; s < c.n_steps; ++s) {
+    const agpm_plan_step& t = c.steps[s];
+    PlanStep st;
+    st.pattern_vertex = t.pattern_vertex;
+    st.in_positions.assign(t.in_positions, t.in_positions + t.n_in);
+    st.out_positions.assign(t.out_positions, t.out_positions + t.n_out);
+    st.greater_than.assign(t.greater_than, t.greater_than + t.n_gt);
+    st.less_than.assign(t.less_than, t.less_than + t.n_lt);
+    st.tree_parent = t.tree_parent;
+    st.verify_edges = pairs(t.n_verify, t.verify_edges);
+    p.steps.push_back(std::move(st));
+  }
+  p.closure_edges = pairs(c.n_closure, c.closure_edges);
+  p.constraints = pairs(c.n_constraints, c.constraints);
+  p.terminal_constraints = pairs(c.n_terminal, c.terminal_constraints);
+  return p;
+}
+inline const char* induced_str(InducedMode m) { return m == InducedMode::Vertex ? "vertex" : "edge"; }
+}  // namespace detail
+
+// parse_pattern_spec (pattern.cpp:130-165)
+inline Pattern parse_pattern_spec(const std::string& spec, const std::string& induced_override = "") {
+  agpm_plan c{};
+  detail::check(agpm_plan_compile(spec.c_str(), induced_override.c_str(), 0, 1, &c));
+  Pattern p = detail::from_c(c, spec).pattern;
+  return p;
+}
+inline Pattern builtin_pattern(const std::string& name) { return parse_pattern_spec(name); }
+inline std::vector<std::string> builtin_pattern_names() {
+  char buf[4096];
+  detail::check(agpm_builtin_pattern_names(buf, sizeof(buf)));
+  std::vector<std::string> out;
+  std::string cur;
+  for (const char* s = buf; *s; ++s) {
+    if (*s == '\n') {
+      out.push_back(cur);
+      cur.clear();
+    } else {
+      cur += *s;
+    }
+  }
+  return out;
+}
+// compile_plan (plan.cpp:57-137)
+inline ExecutionPlan compile_plan(const Pattern& pattern, VerifyMode mode, bool enable_symmetry = true) {
+  agpm_plan c{};
+  std::string spec = pattern.spec;
+  if (spec.empty()) {  // a hand-built Pattern: re-express it as a custom spec (pattern.cpp:130-160)
+    spec = "custom:" + std::to_string(pattern.vertex_count) + ":";
+    for (size_t i = 0; i < pattern.edges.size(); ++i)
+      spec += (i ? "," : "") + std::to_string(pattern.edges[i].first) + "-" + std::to_string(pattern.edges[i].second);
+  }
+  detail::check(agpm_plan_compile(spec.c_str(), detail::induced_str(pattern.induced),
+                                  mode == VerifyMode::Lazy ? 1 : 0, enable_symmetry ? 1 : 0, &c));
+  return detail::from_c(c, spec);
+}
+
+// ------------------------------------------------------------------ csr_graph.hpp
+struct CsrView {
+  uint32_t vertex_count = 0;
+  uint64_t edge_count = 0;
+  const uint64_t* begin = nullptr;
+  const uint64_t* end = nullptr;
+  const uint32_t* neighbors = nullptr;
+  bool oriented = false;
+  std::span<const uint32_t> neighbors_of(uint32_t u) const { return {neighbors + begin[u], neighbors + end[u]}; }
+  uint64_t degree(uint32_t u) const { return end[u] - begin[u]; }
+};
+
+class CsrGraph {
+ public:
+  CsrGraph() = default;
+  explicit CsrGraph(agpm_host_graph* h) : h_(h, &agpm_host_graph_free) {}
+  static CsrGraph from_edges(std::vector<std::pair<uint32_t, uint32_t>> edges, uint32_t min_vertex_count = 0) {
+    std::vector<uint32_t> flat;
+    flat.reserve(2 * edges.size());
+    for (auto [u, v] : edges) {
+      flat.push_back(u);
+      flat.push_back(v);
+    }
+    agpm_host_graph* h = nullptr;
+    detail::check(agpm_host_graph_from_edges(flat.data(), edges.size(), min_vertex_count, &h));
+    return CsrGraph(h);
+  }
+  uint32_t vertex_count() const { return info().n; }
+  uint64_t edge_count() const { return info().m; }
+  bool oriented() const { return info().oriented; }
+  CsrView view() const {
+    const uint64_t* off = nullptr;
+    const uint32_t* nbr = nullptr;
+    detail::check(agpm_host_graph_arrays(h_.get(), &off, &nbr));
+    Info i = info();
+    return {i.n, i.m, off, off + 1, nbr, i.oriented};
+  }
+  agpm_host_graph* handle() const { return h_.get(); }
+
+ private:
+  struct Info {
+    uint32_t n;
+    uint64_t m;
+    bool oriented;
+  };
+  Info info() const {
+    uint32_t n = 0;
+    uint64_t m = 0, arcs = 0, maxd = 0;
+    int o = 0;
+    detail::check(agpm_host_graph_info(h_.get(), &n, &m, &arcs, &o, &maxd));
+    return {n, m, o != 0};
+  }
+  std::shared_ptr<agpm_host_graph> h_;
+};
+
+inline CsrGraph load_graph_auto(const std::string& path) {
+  agpm_host_graph* h = nullptr;
+  detail::check(agpm_host_graph_load(path.c_str(), &h));
+  return CsrGraph(h);
+}
+inline CsrGraph load_binary_csr(const std::string& path) { return load_graph_auto(path); }
+inline void write_binary_csr(const CsrGraph& g, const std::string& path) {
+  detail::check(agpm_host_graph_write_binary(g.handle(), path.c_str()));
+}
+inline CsrGraph orient_by_degree(const CsrGraph& g) {
+  agpm_host_graph* h = nullptr;
+  detail::check(agpm_host_graph_orient_by_degree(g.handle(), &h));
+  return CsrGraph(h);
+}
+
+// ------------------------------------------------------------------ ns_engine.hpp
+struct SampledCount {
+  double value = 0.0;
+  bool hit = false;
+  uint64_t work_units = 0;
+};
+struct OnlinePolicy {
+  uint64_t n_min = 1000;
+  uint64_t max_samples = 1000000000;
+  uint64_t profiled_n_samples = 0;
+};
+struct OnlineResult {
+  ConvergenceReport report;
+  SampleAccumulator accumulator;
+  uint64_t windows = 0;
+  uint64_t work_units = 0;
+};
+
+namespace detail {
+// device mirror cache keyed by the (immutable) view's pointers
+inline agpm_graph* device_view(const CsrView& g) {
+  using Key = std::tuple<const void*, const void*, const void*, uint32_t, uint64_t, bool>;
+  struct Entry {
+    Key key;
+    agpm_graph* dev;
+  };
+  thread_local std::list<Entry> cache;
+  const Key key{g.begin, g.end, g.neighbors, g.vertex_count, g.edge_count, g.oriented};
+  for (auto it = cache.begin(); it != cache.end(); ++it)
+    if (it->key == key) {
+      cache.splice(cache.begin(), cache, it);
+      return cache.front().dev;
+    }
+  const bool plain = g.end == g.begin + 1;
+  uint64_t len = 0;
+  for (uint32_t u = 0; u < g.vertex_count; ++u) len = std::max(len, g.end[u]);
+  agpm_graph* dev = nullptr;
+  check(agpm_graph_upload(g.vertex_count, g.edge_count, g.begin, plain ? nullptr : g.end, g.neighbors, len,
+                          g.oriented, nullptr, &dev));
+  cache.push_front({key, dev});
+  if (cache.size() > 4) {
+    agpm_graph_free(cache.back().dev);
+    cache.pop_back();
+  }
+  return dev;
+}
+}  // namespace detail
+
+// draw_sample (ns_engine.cpp:92-104) for a fresh worker-0 stream CounterRng(seed, 0, id)
+inline SampledCount draw_sample(const CsrView& g, const ExecutionPlan& plan, CounterRng& rng) {
+  if (!rng.fresh() || rng.stream1() != 0)
+    throw std::invalid_argument("device draw_sample takes a fresh CounterRng(seed, 0, sample_id)");
+  double v = 0.0;
+  uint8_t hit = 0;
+  detail::check(agpm_ns_draw(detail::device_view(g), &plan.c, rng.seed(), rng.stream2(), 1, &v, &hit, nullptr,
+                             nullptr));
+  return {v, hit != 0, 0};
+}
+
+// run_fixed_budget (ns_engine.cpp:142-153); streams are the workers = 1 streams
+inline SampleAccumulator run_fixed_budget(const CsrView& g, const ExecutionPlan& plan, uint64_t budget,
+                                          uint64_t seed, int /*workers*/ = 1) {
+  agpm_accumulator a{};
+  detail::check(agpm_ns_fixed_budget(detail::device_view(g), &plan.c, budget, seed, &a, nullptr));
+  return detail::from_c(a);
+}
+
+inline double hit_rate_report(const CsrView& g, const ExecutionPlan& plan, uint64_t sample_budget, uint64_t seed,
+                              int workers = 1) {
+  SampleAccumulator acc = run_fixed_budget(g, plan, sample_budget, seed, workers);
+  return static_cast<double>(acc.hits) / static_cast<double>(acc.n);
+}
+
+// run_ns_online (ns_engine.cpp:106-140), workers = 1 window semantics
+inline OnlineResult run_ns_online(const CsrView& g, const ExecutionPlan& plan, double eps, double delta,
+                                  const OnlinePolicy& policy, uint64_t seed, int /*workers*/ = 1) {
+  agpm_online_policy pol{policy.n_min, policy.max_samples, policy.profiled_n_samples};
+  agpm_online_result r{};
+  detail::check(agpm_ns_online(detail::device_view(g), &plan.c, eps, delta, &pol, seed, &r, nullptr));
+  return {detail::from_c(r.report), detail::from_c(r.accumulator), r.windows, r.work_units};
+}
+
+}  // namespace agpm

@@ -149,6 +149,9 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
                       const uint32_t* neighbors, uint64_t neighbor_len, int oriented, void* stream,
                       agpm_graph** out);
 int agpm_graph_upload_host(const agpm_host_graph* g, void* stream, agpm_graph** out);
+/* page-lock (cudaHostRegister) a host graph's arrays so uploads run at DMA
+ * speed; unpinned automatically by agpm_host_graph_free */
+int agpm_host_graph_pin(agpm_host_graph* g);
 int agpm_graph_free(agpm_graph* g);
 int agpm_graph_info(const agpm_graph* g, uint32_t* n, uint64_t* edge_count, uint64_t* arcs,
                     int* oriented, uint64_t* device_bytes);

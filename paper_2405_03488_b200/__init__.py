@@ -108,6 +108,7 @@ def _declare(L):
         "agpm_gen_rmat": (C.c_int, [A.u32, A.u32, C.c_double, C.c_double, C.c_double, A.u64, C.POINTER(A.P)]),
         "agpm_graph_upload": (C.c_int, [A.u32, A.u64, A.pu64, A.pu64, A.pu32, A.u64, C.c_int, A.P, C.POINTER(A.P)]),
         "agpm_graph_upload_host": (C.c_int, [A.P, A.P, C.POINTER(A.P)]),
+        "agpm_host_graph_pin": (C.c_int, [A.P]),
         "agpm_graph_free": (C.c_int, [A.P]),
         "agpm_graph_info": (C.c_int, [A.P, A.pu32, A.pu64, A.pu64, C.POINTER(C.c_int), A.pu64]),
         "agpm_graph_download": (C.c_int, [A.P, A.pu64, A.pu64, A.pu32]),
@@ -274,6 +275,11 @@ class CsrGraph:
         off = np.ctypeslib.as_array(po, shape=(n + 1,)).copy()
         nbr = np.ctypeslib.as_array(pn, shape=(arcs,)).copy() if arcs else np.zeros(0, np.uint32)
         return off, nbr
+
+    def pin(self):
+        """Page-lock the arrays (cudaHostRegister) so device uploads run at DMA speed."""
+        _check(lib().agpm_host_graph_pin(self._h))
+        return self
 
     def relabel_by_degree(self):
         return CsrGraph._make(lib().agpm_host_graph_relabel_by_degree, self._h)

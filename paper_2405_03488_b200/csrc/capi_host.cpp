@@ -82,7 +82,10 @@ int agpm_host_graph_arrays(const agpm_host_graph* g, const uint64_t** offsets, c
   });
 }
 
-void agpm_host_graph_free(agpm_host_graph* g) { delete g; }
+void agpm_host_graph_free(agpm_host_graph* g) {
+  agpm_b200_unpin_host_graph(g);
+  delete g;
+}
 
 int agpm_host_graph_relabel_by_degree(const agpm_host_graph* g, agpm_host_graph** out) {
   return guarded([&] {

@@ -50,4 +50,6 @@ HostGraph gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, dou
 // C-ABI opaque handle (agpm_b200.h)
 struct agpm_host_graph {
   agpm_b200::HostGraph g;
+  bool pinned = false;
 };
+void agpm_b200_unpin_host_graph(agpm_host_graph* g);

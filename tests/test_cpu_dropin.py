@@ -1,0 +1,35 @@
+"""CPU: a reference-style C++ caller compiles against include/agpm/agpm.hpp,
+links libagpm_b200.so and gets the reference's answers for the host parts."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _build(tmp_path):
+    exe = str(tmp_path / "dropin")
+    lib = os.path.join(ROOT, "paper_2405_03488_b200")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "dropin_host.cpp"), "-L", lib, "-lagpm_b200",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    return exe
+
+
+def test_dropin_header_host_calls(agpm, tmp_path):
+    out = subprocess.run([_build(tmp_path)], check=True, capture_output=True, text=True).stdout
+    assert "plan 4clique k=4 steps=2 seed_ordered=1 rule='m * |S_2| * |S_3|'" in out
+    assert "hand-built 4-cycle rule='m * |S_2| * |S_3|'" in out
+    assert "pattern_error ok" in out
+    assert "graph n=4 m=6" in out
+    assert "eps_hat=1.38590" in out  # test_ns_engine.cpp:86
+
+
+@pytest.mark.gpu
+def test_dropin_header_device_calls(agpm, tmp_path):
+    out = subprocess.run([_build(tmp_path), "--device"], check=True, capture_output=True, text=True).stdout
+    import re
+    est = float(re.search(r"K4 4-cliques ~ ([0-9.]+)", out).group(1))
+    assert abs(est - 1.0) < 0.1  # K4 holds exactly one 4-clique; eps = 5 %
+    assert "converged=1" in out
