@@ -213,6 +213,12 @@ int agpm_window_moments_dev(const double* d_values, uint64_t count, uint64_t win
 int agpm_ns_bmin_bytes(agpm_graph* g, const agpm_plan* plan, uint64_t seed, uint64_t first_id,
                        uint64_t count, uint64_t* total_bytes, void* stream);
 
+/* ------------------------------------------------- exact counting ---------
+ * exact_count (exact_engine.cpp:66-91) for eager plans: oriented clique views
+ * skip the order bounds (every arc is a seed), symmetric views apply them and
+ * skip u > v seeds when the plan orients the seed edge. */
+int agpm_exact_count(agpm_graph* g, const agpm_plan* plan, uint64_t* count, void* stream);
+
 /* ------------------------------------------------------- misc / device -----*/
 const char* agpm_last_error(void);
 int agpm_device_count(int* n);

@@ -26,7 +26,7 @@ __all__ = [
     "lib", "compile_plan", "builtin_pattern_names", "automorphism_count", "scaling_rule_text",
     "plan_verifies_each_edge_once", "norm_cdf", "inv_norm_cdf", "predicted_error", "CsrGraph",
     "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
-    "hit_rate_report", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "hit_rate_report", "exact_count", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
 ]
 
@@ -120,6 +120,7 @@ def _declare(L):
         "agpm_window_moments_dev": (C.c_int, [A.P, A.u64, A.u64, A.P, A.P]),
         "agpm_ns_bmin_bytes": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pu64, A.P]),
         "agpm_ns_set_strategy": (C.c_int, [C.c_int]),
+        "agpm_exact_count": (C.c_int, [A.P, A.pPlan, A.pu64, A.P]),
         "agpm_ns_set_frontier_reuse": (C.c_int, [C.c_int]),
     }
     for name, (res, args) in sig.items():
@@ -363,6 +364,13 @@ def run_ns_online(dg, plan, eps, delta, policy=None, seed=1, workers=1, stream=N
     pol = policy if policy is not None else OnlinePolicy()
     _check(lib().agpm_ns_online(dg._h, C.byref(plan), eps, delta, C.byref(pol), seed, C.byref(res), stream))
     return res
+
+
+def exact_count(dg, plan, threads=1, stream=None):
+    """exact_count (exact_engine.cpp:66-91) on the device; eager plans."""
+    out = C.c_uint64()
+    _check(lib().agpm_exact_count(dg._h, C.byref(plan), C.byref(out), stream))
+    return out.value
 
 
 def bmin_bytes(dg, plan, seed, first_id, count, stream=None):
