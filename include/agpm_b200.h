@@ -155,6 +155,8 @@ int agpm_host_graph_pin(agpm_host_graph* g);
 int agpm_graph_free(agpm_graph* g);
 int agpm_graph_info(const agpm_graph* g, uint32_t* n, uint64_t* edge_count, uint64_t* arcs,
                     int* oriented, uint64_t* device_bytes);
+/* length of the view's neighbour array (>= its arc count for split views) */
+int agpm_graph_neighbor_len(const agpm_graph* g, uint64_t* len);
 /* copy the view back to host (tests): begin[n], end[n], neighbors[neighbor_len] */
 int agpm_graph_download(const agpm_graph* g, uint64_t* begin, uint64_t* end, uint32_t* neighbors);
 
@@ -218,6 +220,29 @@ int agpm_ns_bmin_bytes(agpm_graph* g, const agpm_plan* plan, uint64_t seed, uint
  * skip the order bounds (every arc is a seed), symmetric views apply them and
  * skip u > v seeds when the plan orients the seed edge. */
 int agpm_exact_count(agpm_graph* g, const agpm_plan* plan, uint64_t* count, void* stream);
+
+/* ------------------------------------------- sparsification and GS -------
+ * colour split: ColoredCsr::color_vertices (colored_csr.cpp:48-54) -> the
+ *   zero-copy same-colour view (begin = offsets, end = split ends, colored_csr.cpp:90-93);
+ *   colors_out (nullable, host) receives the n vertex colours.
+ * Bernoulli: bernoulli_sparsify (csr_graph.cpp:190-213), a new plain CSR.
+ * gs_estimate (gs_engine.cpp:42-75): scheme 0 = Bernoulli edge (scale p^-l),
+ *   1 = colour (scale c^(k-1)); raw count from agpm_exact_count. */
+typedef struct agpm_gs_result {
+  double estimate;
+  uint64_t raw_count;
+  double scale;
+  double preprocess_seconds, search_seconds;
+} agpm_gs_result;
+
+int agpm_color_split(agpm_graph* g, uint32_t colors, uint64_t seed, uint32_t* colors_out, uint64_t* same_edges,
+                     agpm_graph** out, void* stream);
+int agpm_bernoulli_sparsify(agpm_graph* g, double keep_probability, uint64_t seed, agpm_graph** out,
+                            void* stream);
+int agpm_gs_estimate(agpm_graph* g, const agpm_plan* plan, int scheme, double keep_probability, uint32_t colors,
+                     uint64_t seed, agpm_gs_result* out, void* stream);
+/* triangle_count (csr_graph.cpp:225-239) */
+int agpm_triangle_count(agpm_graph* g, uint64_t* count, void* stream);
 
 /* ------------------------------------------------------- misc / device -----*/
 const char* agpm_last_error(void);

@@ -26,7 +26,7 @@ __all__ = [
     "lib", "compile_plan", "builtin_pattern_names", "automorphism_count", "scaling_rule_text",
     "plan_verifies_each_edge_once", "norm_cdf", "inv_norm_cdf", "predicted_error", "CsrGraph",
     "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
-    "hit_rate_report", "exact_count", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "hit_rate_report", "exact_count", "gs_estimate", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
 ]
 
@@ -112,6 +112,7 @@ def _declare(L):
         "agpm_graph_free": (C.c_int, [A.P]),
         "agpm_graph_info": (C.c_int, [A.P, A.pu32, A.pu64, A.pu64, C.POINTER(C.c_int), A.pu64]),
         "agpm_graph_download": (C.c_int, [A.P, A.pu64, A.pu64, A.pu32]),
+        "agpm_graph_neighbor_len": (C.c_int, [A.P, A.pu64]),
         "agpm_ns_draw": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pdbl, A.pu8, A.pu32, A.P]),
         "agpm_ns_fixed_budget": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.pAcc, A.P]),
         "agpm_ns_online": (C.c_int, [A.P, A.pPlan, C.c_double, C.c_double, C.POINTER(OnlinePolicy), A.u64,
@@ -121,6 +122,10 @@ def _declare(L):
         "agpm_ns_bmin_bytes": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pu64, A.P]),
         "agpm_ns_set_strategy": (C.c_int, [C.c_int]),
         "agpm_exact_count": (C.c_int, [A.P, A.pPlan, A.pu64, A.P]),
+        "agpm_color_split": (C.c_int, [A.P, A.u32, A.u64, A.pu32, A.pu64, C.POINTER(A.P), A.P]),
+        "agpm_bernoulli_sparsify": (C.c_int, [A.P, C.c_double, A.u64, C.POINTER(A.P), A.P]),
+        "agpm_gs_estimate": (C.c_int, [A.P, A.pPlan, C.c_int, C.c_double, A.u32, A.u64, C.POINTER(A.GsResult), A.P]),
+        "agpm_triangle_count": (C.c_int, [A.P, A.pu64, A.P]),
         "agpm_ns_set_frontier_reuse": (C.c_int, [C.c_int]),
     }
     for name, (res, args) in sig.items():
@@ -307,9 +312,11 @@ class DeviceGraph:
     """Device-resident CsrView mirror (agpm_graph)."""
 
     def __init__(self, graph=None, *, begin=None, end=None, neighbors=None, vertex_count=None, edge_count=None,
-                 oriented=False, stream=None):
+                 oriented=False, stream=None, _handle=None):
         h = C.c_void_p()
-        if graph is not None:
+        if _handle is not None:
+            h = _handle
+        elif graph is not None:
             _check(lib().agpm_graph_upload_host(graph._h, stream, C.byref(h)))
         else:
             b = np.ascontiguousarray(begin, dtype=np.uint64)
@@ -326,6 +333,36 @@ class DeviceGraph:
         if h and h.value and _lib is not None:
             _lib.agpm_graph_free(h)
             self._h = None
+
+    def download(self):
+        """(begin u64[n], end u64[n], neighbors u32[neighbor_len]) of the view (tests)."""
+        n = self.info()["vertex_count"]
+        nl = C.c_uint64()
+        _check(lib().agpm_graph_neighbor_len(self._h, C.byref(nl)))
+        b = np.zeros(max(n, 1), np.uint64)
+        e = np.zeros(max(n, 1), np.uint64)
+        nb = np.zeros(max(nl.value, 1), np.uint32)
+        _check(lib().agpm_graph_download(self._h, _ptr(b, C.c_uint64), _ptr(e, C.c_uint64), _ptr(nb, C.c_uint32)))
+        return b[:n], e[:n], nb[: nl.value]
+
+    def color_split(self, colors, seed, stream=None):
+        """ColoredCsr::color_vertices -> (same-colour view, host colours, same-colour edge count)."""
+        n = self.info()["vertex_count"]
+        cols = np.zeros(max(n, 1), np.uint32)
+        same = C.c_uint64()
+        h = C.c_void_p()
+        _check(lib().agpm_color_split(self._h, colors, seed, _ptr(cols, C.c_uint32), C.byref(same), C.byref(h), stream))
+        return DeviceGraph(_handle=h), cols[:n], same.value
+
+    def bernoulli_sparsify(self, keep_probability, seed, stream=None):
+        h = C.c_void_p()
+        _check(lib().agpm_bernoulli_sparsify(self._h, keep_probability, seed, C.byref(h), stream))
+        return DeviceGraph(_handle=h)
+
+    def triangle_count(self, stream=None):
+        out = C.c_uint64()
+        _check(lib().agpm_triangle_count(self._h, C.byref(out), stream))
+        return out.value
 
     def info(self):
         n, m, arcs, o, by = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_int(), C.c_uint64()
@@ -371,6 +408,14 @@ def exact_count(dg, plan, threads=1, stream=None):
     out = C.c_uint64()
     _check(lib().agpm_exact_count(dg._h, C.byref(plan), C.byref(out), stream))
     return out.value
+
+
+def gs_estimate(dg, plan, scheme="color", keep_probability=1.0, colors=1, seed=0, threads=1, stream=None):
+    """gs_estimate (gs_engine.cpp:42-75): scheme "color" (scale c^(k-1)) or "bernoulli" (scale p^-l)."""
+    out = _abi.GsResult()
+    _check(lib().agpm_gs_estimate(dg._h, C.byref(plan), {"bernoulli": 0, "color": 1}[scheme], keep_probability,
+                                  colors, seed, C.byref(out), stream))
+    return out
 
 
 def bmin_bytes(dg, plan, seed, first_id, count, stream=None):

@@ -111,6 +111,11 @@ class OnlineResult(C.Structure):
                 ("work_units", C.c_uint64), ("samples_launched", C.c_uint64), ("seconds", C.c_double)]
 
 
+class GsResult(C.Structure):
+    _fields_ = [("estimate", C.c_double), ("raw_count", C.c_uint64), ("scale", C.c_double),
+                ("preprocess_seconds", C.c_double), ("search_seconds", C.c_double)]
+
+
 P = C.c_void_p
 u32, u64, i32, dbl = C.c_uint32, C.c_uint64, C.c_int, C.c_double
 pu32, pu64, pdbl, pu8 = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_uint8)

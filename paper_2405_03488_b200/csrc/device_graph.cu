@@ -242,6 +242,13 @@ int agpm_graph_info(const agpm_graph* g, uint32_t* n, uint64_t* edge_count, uint
   });
 }
 
+int agpm_graph_neighbor_len(const agpm_graph* g, uint64_t* len) {
+  return guarded([&] {
+    if (!g || !len) throw std::invalid_argument("null argument");
+    *len = g->nbr_len;
+  });
+}
+
 int agpm_graph_download(const agpm_graph* g, uint64_t* begin, uint64_t* end, uint32_t* neighbors) {
   return guarded([&] {
     std::vector<VtxInfo> v(g->n);
