@@ -155,6 +155,8 @@ int agpm_host_graph_pin(agpm_host_graph* g);
 int agpm_graph_free(agpm_graph* g);
 int agpm_graph_info(const agpm_graph* g, uint32_t* n, uint64_t* edge_count, uint64_t* arcs,
                     int* oriented, uint64_t* device_bytes);
+/* CsrView::max_degree (csr_graph.cpp:21-25) of the device view */
+int agpm_graph_max_degree(const agpm_graph* g, uint64_t* out);
 /* length of the view's neighbour array (>= its arc count for split views) */
 int agpm_graph_neighbor_len(const agpm_graph* g, uint64_t* len);
 /* copy the view back to host (tests): begin[n], end[n], neighbors[neighbor_len] */
@@ -243,6 +245,67 @@ int agpm_gs_estimate(agpm_graph* g, const agpm_plan* plan, int scheme, double ke
                      uint64_t seed, agpm_gs_result* out, void* stream);
 /* triangle_count (csr_graph.cpp:225-239) */
 int agpm_triangle_count(agpm_graph* g, uint64_t* count, void* stream);
+
+/* --------------------------------------------- hybrid scheme choice -------
+ * keep probability (gs_engine.cpp:24-40), NS cost cone (cost_model.cpp:78-110),
+ * GS cost model (:112-145), fast profiler (:147-190, on device), selector
+ * (:192-194), gamma probing (gs_engine.cpp:179-197 + exact_engine.cpp:135-213,
+ * host), and the CLI's loose-mode orchestration (agpm_main.cpp:221-287). */
+typedef struct agpm_keep_probability {
+  double p;
+  int32_t sparsification_useless;
+  uint32_t color_count; /* floor(1/p), >= 1 */
+} agpm_keep_probability;
+
+typedef struct agpm_cost_cone {
+  double lower_slope, upper_slope;
+  uint64_t n_samples;
+  double lower_time, upper_time;
+} agpm_cost_cone;
+
+typedef struct agpm_gs_cost {
+  double preprocess_work, search_work, total_seconds;
+  uint32_t color_count;
+} agpm_gs_cost;
+
+typedef struct agpm_profile_result {
+  double n_samples_estimate, mu_prime, scaled_count, epsilon_hat_final;
+  uint64_t n_converged;
+  double fraction;
+  int32_t reliable;
+  double seconds;
+} agpm_profile_result;
+
+typedef struct agpm_hybrid_result {
+  int32_t decision; /* 0 = NS (strict), 1 = GS */
+  double estimate;
+  double gamma;
+  agpm_profile_result profile;
+  agpm_keep_probability keep;
+  agpm_cost_cone cone;
+  agpm_gs_cost gs_model;
+  agpm_gs_result gs;
+  agpm_online_result ns;
+} agpm_hybrid_result;
+
+int agpm_choose_keep_probability(double eps, double delta, double count_estimate, double gamma_estimate,
+                                 agpm_keep_probability* out);
+int agpm_ns_cost_cone(double vertex_count, double arc_count, const agpm_plan* plan, uint64_t n_samples,
+                      double hw_const, agpm_cost_cone* out);
+int agpm_gs_cost_estimate(double vertex_count, double edge_count, const agpm_plan* plan, uint32_t colors,
+                          double hw_const, uint64_t triangle_count, agpm_gs_cost* out);
+int agpm_select_scheme(const agpm_cost_cone* cone, const agpm_gs_cost* gs); /* 1 = GS */
+int agpm_count_matches_through_edge(const agpm_host_graph* g, const agpm_plan* plan, uint32_t u, uint32_t v,
+                                    uint64_t* out);
+int agpm_estimate_gamma(const agpm_host_graph* g, const agpm_plan* plan, uint64_t probe_edges, uint64_t seed,
+                        int64_t work_budget, uint64_t* out);
+int agpm_fast_profile(agpm_graph* g, const agpm_plan* plan, double profile_fraction, double user_epsilon,
+                      uint64_t seed, uint64_t profiler_sample_cap, agpm_profile_result* out, void* stream);
+/* device analogue of calibrate_hardware_constant (cost_model.cpp:31-76): seconds
+ * per cone work unit of the device sampler on a synthetic graph */
+int agpm_calibrate_hardware_constant(double* out);
+int agpm_count_hybrid(const agpm_host_graph* hg, agpm_graph* g, const agpm_plan* plan, double eps, double confidence,
+                      uint64_t seed, double profile_fraction, double hw_const, agpm_hybrid_result* out, void* stream);
 
 /* ------------------------------------------------------- misc / device -----*/
 const char* agpm_last_error(void);

@@ -26,7 +26,9 @@ __all__ = [
     "lib", "compile_plan", "builtin_pattern_names", "automorphism_count", "scaling_rule_text",
     "plan_verifies_each_edge_once", "norm_cdf", "inv_norm_cdf", "predicted_error", "CsrGraph",
     "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
-    "hit_rate_report", "exact_count", "gs_estimate", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "hit_rate_report", "exact_count", "gs_estimate", "choose_keep_probability", "ns_cost_cone",
+    "gs_cost_estimate", "select_scheme", "count_matches_through_edge", "estimate_gamma", "fast_profile",
+    "calibrate_hardware_constant", "count_hybrid", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
 ]
 
@@ -126,6 +128,19 @@ def _declare(L):
         "agpm_bernoulli_sparsify": (C.c_int, [A.P, C.c_double, A.u64, C.POINTER(A.P), A.P]),
         "agpm_gs_estimate": (C.c_int, [A.P, A.pPlan, C.c_int, C.c_double, A.u32, A.u64, C.POINTER(A.GsResult), A.P]),
         "agpm_triangle_count": (C.c_int, [A.P, A.pu64, A.P]),
+        "agpm_graph_max_degree": (C.c_int, [A.P, A.pu64]),
+        "agpm_choose_keep_probability": (C.c_int, [C.c_double] * 4 + [C.POINTER(A.KeepProbability)]),
+        "agpm_ns_cost_cone": (C.c_int, [C.c_double, C.c_double, A.pPlan, A.u64, C.c_double, C.POINTER(A.CostCone)]),
+        "agpm_gs_cost_estimate": (C.c_int, [C.c_double, C.c_double, A.pPlan, A.u32, C.c_double, A.u64,
+                                            C.POINTER(A.GsCost)]),
+        "agpm_select_scheme": (C.c_int, [C.POINTER(A.CostCone), C.POINTER(A.GsCost)]),
+        "agpm_count_matches_through_edge": (C.c_int, [A.P, A.pPlan, A.u32, A.u32, A.pu64]),
+        "agpm_estimate_gamma": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, C.c_int64, A.pu64]),
+        "agpm_fast_profile": (C.c_int, [A.P, A.pPlan, C.c_double, C.c_double, A.u64, A.u64,
+                                        C.POINTER(A.ProfileResult), A.P]),
+        "agpm_calibrate_hardware_constant": (C.c_int, [A.pdbl]),
+        "agpm_count_hybrid": (C.c_int, [A.P, A.P, A.pPlan, C.c_double, C.c_double, A.u64, C.c_double, C.c_double,
+                                        C.POINTER(A.HybridResult), A.P]),
         "agpm_ns_set_frontier_reuse": (C.c_int, [C.c_int]),
     }
     for name, (res, args) in sig.items():
@@ -415,6 +430,70 @@ def gs_estimate(dg, plan, scheme="color", keep_probability=1.0, colors=1, seed=0
     out = _abi.GsResult()
     _check(lib().agpm_gs_estimate(dg._h, C.byref(plan), {"bernoulli": 0, "color": 1}[scheme], keep_probability,
                                   colors, seed, C.byref(out), stream))
+    return out
+
+
+# ------------------------------------------------------------------ hybrid scheme choice
+def choose_keep_probability(eps, delta, count_estimate, gamma_estimate):
+    """choose_keep_probability (gs_engine.cpp:24-40) -> KeepProbability(p, sparsification_useless, color_count)."""
+    out = _abi.KeepProbability()
+    _check(lib().agpm_choose_keep_probability(eps, delta, count_estimate, gamma_estimate, C.byref(out)))
+    return out
+
+
+def ns_cost_cone(vertex_count, arc_count, plan, n_samples, hw_const):
+    """ns_cost_cone (cost_model.cpp:92-110); average degree = arc_count / vertex_count."""
+    out = _abi.CostCone()
+    _check(lib().agpm_ns_cost_cone(vertex_count, arc_count, C.byref(plan), n_samples, hw_const, C.byref(out)))
+    return out
+
+
+def gs_cost_estimate(vertex_count, edge_count, plan, colors, hw_const, triangle_count):
+    """gs_cost_estimate (cost_model.cpp:112-145)."""
+    out = _abi.GsCost()
+    _check(lib().agpm_gs_cost_estimate(vertex_count, edge_count, C.byref(plan), colors, hw_const, triangle_count,
+                                       C.byref(out)))
+    return out
+
+
+def select_scheme(cone, gs):
+    """select_scheme (cost_model.cpp:192-194): "gs" below the cone, else "ns"."""
+    return "gs" if lib().agpm_select_scheme(C.byref(cone), C.byref(gs)) == 1 else "ns"
+
+
+def count_matches_through_edge(graph, plan, u, v):
+    out = C.c_uint64()
+    _check(lib().agpm_count_matches_through_edge(graph._h, C.byref(plan), u, v, C.byref(out)))
+    return out.value
+
+
+def estimate_gamma(graph, plan, probe_edges, seed, work_budget=50000000):
+    """estimate_gamma (gs_engine.cpp:179-197) on the host CSR."""
+    out = C.c_uint64()
+    _check(lib().agpm_estimate_gamma(graph._h, C.byref(plan), probe_edges, seed, work_budget, C.byref(out)))
+    return out.value
+
+
+def fast_profile(dg, plan, profile_fraction, user_epsilon, seed, profiler_sample_cap=1000000, stream=None):
+    """fast_profile (cost_model.cpp:147-190): device Bernoulli sparsify + device online NS."""
+    out = _abi.ProfileResult()
+    _check(lib().agpm_fast_profile(dg._h, C.byref(plan), profile_fraction, user_epsilon, seed, profiler_sample_cap,
+                                   C.byref(out), stream))
+    return out
+
+
+def calibrate_hardware_constant():
+    out = C.c_double()
+    _check(lib().agpm_calibrate_hardware_constant(C.byref(out)))
+    return out.value
+
+
+def count_hybrid(graph, dg, plan, eps, confidence, seed, profile_fraction=0.1, hw_const=1e-9, stream=None):
+    """The CLI's loose mode (agpm_main.cpp:221-287): profile, gamma, keep probability, both cost
+    models, select NS or GS, run it. Returns HybridResult (decision 0 = NS, 1 = GS)."""
+    out = _abi.HybridResult()
+    _check(lib().agpm_count_hybrid(graph._h, dg._h, C.byref(plan), eps, confidence, seed, profile_fraction, hw_const,
+                                   C.byref(out), stream))
     return out
 
 

@@ -116,6 +116,32 @@ class GsResult(C.Structure):
                 ("preprocess_seconds", C.c_double), ("search_seconds", C.c_double)]
 
 
+class KeepProbability(C.Structure):
+    _fields_ = [("p", C.c_double), ("sparsification_useless", C.c_int32), ("color_count", C.c_uint32)]
+
+
+class CostCone(C.Structure):
+    _fields_ = [("lower_slope", C.c_double), ("upper_slope", C.c_double), ("n_samples", C.c_uint64),
+                ("lower_time", C.c_double), ("upper_time", C.c_double)]
+
+
+class GsCost(C.Structure):
+    _fields_ = [("preprocess_work", C.c_double), ("search_work", C.c_double), ("total_seconds", C.c_double),
+                ("color_count", C.c_uint32)]
+
+
+class ProfileResult(C.Structure):
+    _fields_ = [("n_samples_estimate", C.c_double), ("mu_prime", C.c_double), ("scaled_count", C.c_double),
+                ("epsilon_hat_final", C.c_double), ("n_converged", C.c_uint64), ("fraction", C.c_double),
+                ("reliable", C.c_int32), ("seconds", C.c_double)]
+
+
+class HybridResult(C.Structure):
+    _fields_ = [("decision", C.c_int32), ("estimate", C.c_double), ("gamma", C.c_double),
+                ("profile", ProfileResult), ("keep", KeepProbability), ("cone", CostCone), ("gs_model", GsCost),
+                ("gs", GsResult), ("ns", OnlineResult)]
+
+
 P = C.c_void_p
 u32, u64, i32, dbl = C.c_uint32, C.c_uint64, C.c_int, C.c_double
 pu32, pu64, pdbl, pu8 = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_uint8)

@@ -242,6 +242,13 @@ int agpm_graph_info(const agpm_graph* g, uint32_t* n, uint64_t* edge_count, uint
   });
 }
 
+int agpm_graph_max_degree(const agpm_graph* g, uint64_t* out) {
+  return guarded([&] {
+    if (!g || !out) throw std::invalid_argument("null argument");
+    *out = g->max_degree;
+  });
+}
+
 int agpm_graph_neighbor_len(const agpm_graph* g, uint64_t* len) {
   return guarded([&] {
     if (!g || !len) throw std::invalid_argument("null argument");
