@@ -370,10 +370,12 @@ __device__ __forceinline__ bool warp_contains(uint32_t b, uint32_t a) {
   return __shfl_sync(FULL, b, pos) == a;
 }
 
-// Warps own contiguous sample ranges and walk every bitmap word of each owned
-// sample (a word = 32 driver elements of ONE sample). A sample's descriptor and
-// the 32 splitters of each of its other lists stay in registers across its
-// words, so a word costs: one coalesced driver load, per list a 5-step shuffle
+// Warps own contiguous runs of bitmap words (balanced however skewed the
+// per-sample word counts are); a word = 32 driver elements of ONE sample. The
+// owning sample is found once per run (k-ary search over the word offsets) and
+// advanced as the run crosses sample boundaries; while consecutive words stay
+// in one sample its descriptor and the 32 splitters of each other list stay in
+// registers. A word costs one coalesced driver load, per list a 5-step shuffle
 // bucket search + a fixed-trip branchless search inside the bucket, one ballot.
 template <int K>
 __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, unsigned long long words) {
@@ -383,12 +385,26 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
   const uint32_t* __restrict__ nbr = A.g.nbr;
   const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
   const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-  const unsigned long long per = (A.count + nwarps - 1) / nwarps;
-  const unsigned long long s0 = warp * per, s1 = min(A.count, s0 + per);
-  (void)words;
-  for (unsigned long long s = s0; s < s1; ++s) {
-    const unsigned long long w0 = off[s], w1 = off[s + 1];
-    if (w0 == w1) continue;  // not pending at this step
+  const unsigned long long per = (words + nwarps - 1) / nwarps;
+  const unsigned long long w_begin = warp * per, w_end = min(words, w_begin + per);
+  if (w_begin >= w_end) return;
+  unsigned long long s;
+  {  // last s with off[s] <= w_begin
+    unsigned long long lo = 0, hi = A.count;
+    while (hi - lo > 32) {
+      const unsigned long long stp = (hi - lo) / 33;
+      const unsigned c = __popc(__ballot_sync(FULL, off[lo + (unsigned long long)(lane + 1) * stp] <= w_begin));
+      const unsigned long long nlo = c ? lo + c * stp : lo;
+      hi = c < 32 ? lo + (c + 1) * stp : hi;
+      lo = nlo;
+    }
+    const unsigned long long pos = lo + lane;
+    s = lo + __popc(__ballot_sync(FULL, pos < hi && off[pos] <= w_begin)) - 1;
+  }
+  unsigned long long w = w_begin;
+  while (w < w_end) {
+    while (off[s + 1] <= w) ++s;  // uniform
+    const unsigned long long ws = off[s], we = min(off[s + 1], w_end);
     const IsectDesc<K>& d = desc[s];
     const uint32_t dsize = d.dsize, lists = d.lists, outs = d.outs;
     const uint32_t* D = d.drv;
@@ -407,8 +423,8 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
         sp[q] = (uint32_t)lane < nb[q] || nb[q] > 32 ? ldn(B[q], at) : INF;
       }
     }
-    for (unsigned long long w = w0; w < w1; ++w) {
-      const uint32_t o = (uint32_t)(w - w0) * 32 + lane;
+    for (; w < we; ++w) {
+      const uint32_t o = (uint32_t)(w - ws) * 32 + lane;
       const bool valid = o < dsize;
       const uint32_t a = valid ? ldn(D, o) : INF;
       bool fail = false;
@@ -661,7 +677,7 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
           A.survivors[slot] = static_cast<uint32_t*>(ctx.get(10 + slot, 4 * A.surv_cap + 64));
           AGPM_CUDA(cudaMemsetAsync(A.surv_cursor + slot, 0, 8, s));
         }
-        const unsigned long long warps = std::min<unsigned long long>(c, (unsigned long long)sms * 64);
+        const unsigned long long warps = std::min<unsigned long long>(words, (unsigned long long)sms * 64);
         fr_isect_kernel<K><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(A, words);
         count_launch();
         AGPM_CUDA(cudaGetLastError());
