@@ -370,13 +370,8 @@ __device__ __forceinline__ bool warp_contains(uint32_t b, uint32_t a) {
   return __shfl_sync(FULL, b, pos) == a;
 }
 
-// Warps own contiguous runs of bitmap words (balanced however skewed the
-// per-sample word counts are); a word = 32 driver elements of ONE sample. The
-// owning sample is found once per run (k-ary search over the word offsets) and
-// advanced as the run crosses sample boundaries; while consecutive words stay
-// in one sample its descriptor and the 32 splitters of each other list stay in
-// registers. A word costs one coalesced driver load, per list a 5-step shuffle
-// bucket search + a fixed-trip branchless search inside the bucket, one ballot.
+// One warp per bitmap word; warps walk contiguous word runs so the owning
+// sample is found once (k-ary over the word offsets) and then advanced.
 template <int K>
 __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, unsigned long long words) {
   const int lane = threadIdx.x & 31;
@@ -386,80 +381,59 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
   const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
   const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
   const unsigned long long per = (words + nwarps - 1) / nwarps;
-  const unsigned long long w_begin = warp * per, w_end = min(words, w_begin + per);
-  if (w_begin >= w_end) return;
+  const unsigned long long w0 = warp * per, w1 = min(words, w0 + per);
+  if (w0 >= w1) return;
   unsigned long long s;
-  {  // last s with off[s] <= w_begin
+  {  // last s with off[s] <= w0
     unsigned long long lo = 0, hi = A.count;
     while (hi - lo > 32) {
-      const unsigned long long stp = (hi - lo) / 33;
-      const unsigned c = __popc(__ballot_sync(FULL, off[lo + (unsigned long long)(lane + 1) * stp] <= w_begin));
-      const unsigned long long nlo = c ? lo + c * stp : lo;
-      hi = c < 32 ? lo + (c + 1) * stp : hi;
+      const unsigned long long step = (hi - lo) / 33;
+      const unsigned c = __popc(__ballot_sync(FULL, off[lo + (unsigned long long)(lane + 1) * step] <= w0));
+      const unsigned long long nlo = c ? lo + c * step : lo;
+      hi = c < 32 ? lo + (c + 1) * step : hi;
       lo = nlo;
     }
     const unsigned long long pos = lo + lane;
-    s = lo + __popc(__ballot_sync(FULL, pos < hi && off[pos] <= w_begin)) - 1;
+    s = lo + __popc(__ballot_sync(FULL, pos < hi && off[pos] <= w0)) - 1;
   }
-  unsigned long long w = w_begin;
-  while (w < w_end) {
+  for (unsigned long long w = w0; w < w1; ++w) {
     while (off[s + 1] <= w) ++s;  // uniform
-    const unsigned long long ws = off[s], we = min(off[s + 1], w_end);
     const IsectDesc<K>& d = desc[s];
-    const uint32_t dsize = d.dsize, lists = d.lists, outs = d.outs;
-    const uint32_t* D = d.drv;
-    const uint32_t* B[K - 1];
-    uint32_t nb[K - 1], step[K - 1], sp[K - 1];
+    const uint32_t o = (uint32_t)(w - off[s]) * 32 + lane;
+    const bool valid = o < d.dsize;
+    const uint32_t a = valid ? ldn(d.drv, o) : INF;
+    bool fail = false;
 #pragma unroll
     for (int q = 0; q < K - 1; ++q) {
-      B[q] = nbr;
-      nb[q] = step[q] = sp[q] = 0;
-      if ((lists >> q) & 1u) {
-        B[q] = nbr + d.start[q];
-        nb[q] = d.len[q];
-        // lists <= 32: the whole list in registers; else 32 splitters at (i+1)*step
-        step[q] = nb[q] <= 32 ? 0 : nb[q] / 33u;
-        const uint32_t at = nb[q] <= 32 ? (uint32_t)lane : (uint32_t)(lane + 1) * step[q];
-        sp[q] = (uint32_t)lane < nb[q] || nb[q] > 32 ? ldn(B[q], at) : INF;
-      }
-    }
-    for (; w < we; ++w) {
-      const uint32_t o = (uint32_t)(w - ws) * 32 + lane;
-      const bool valid = o < dsize;
-      const uint32_t a = valid ? ldn(D, o) : INF;
-      bool fail = false;
-#pragma unroll
-      for (int q = 0; q < K - 1; ++q) {
-        if (!((lists >> q) & 1u)) continue;
-        int c = 0;  // #register values < a
+      if (!((d.lists >> q) & 1u)) continue;
+      bool found;
+      const uint32_t* B = nbr + d.start[q];
+      const uint32_t nb = d.len[q];
+      if (A.g.ehash) {
+        // a is inside [lo, hi) already, so membership in the restricted list is edge existence
+        found = valid && edge_lookup(A.g.ehash, A.g.ehash_mask, a, d.owner[q]);
+      } else if (nb <= 32) {
+        found = warp_contains((uint32_t)lane < nb ? ldn(B, lane) : INF, a);
+      } else {
+        // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then a short per-lane search
+        const uint32_t step = nb / 33u;
+        const uint32_t sp = ldn(B, (uint32_t)(lane + 1) * step);
+        int c = 0;
 #pragma unroll
         for (int sh = 16; sh >= 1; sh >>= 1) {
-          const uint32_t t = __shfl_sync(FULL, sp[q], c + sh - 1);
+          const uint32_t t = __shfl_sync(FULL, sp, c + sh - 1);
           if (t < a) c += sh;
         }
-        const uint32_t tc = __shfl_sync(FULL, sp[q], c);
-        bool found;
-        if (step[q] == 0) {
-          found = tc == a;
-        } else {
-          c += tc < a ? 1 : 0;
-          // lower_bound(a) lies in [lo, hi]; branchless search over [lo, hi)
-          uint32_t lo = c ? (uint32_t)c * step[q] + 1 : 0;
-          const uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step[q] : nb[q];
-          uint32_t n = hi - lo;
-          while (n > 1) {
-            const uint32_t half = n >> 1;
-            lo = ldn(B[q], lo + half - 1) < a ? lo + half : lo;
-            n -= half;
-          }
-          if (n == 1 && ldn(B[q], lo) < a) ++lo;
-          found = lo < nb[q] && ldn(B[q], lo) == a;
-        }
-        fail = fail || (found == (bool)((outs >> q) & 1u));
+        c += __shfl_sync(FULL, sp, c) < a ? 1 : 0;  // c = #splitters < a, in [0, 32]
+        const uint32_t lo = c ? (uint32_t)c * step + 1 : 0;
+        const uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step : nb;
+        const uint32_t at = lb_thread(B, lo, hi, a);
+        found = at < nb && ldn(B, at) == a;
       }
-      const unsigned bal = __ballot_sync(FULL, valid && fail);
-      if (lane == 0) A.bitmap[w] = bal;
+      fail = fail || (found == (bool)((d.outs >> q) & 1u));
     }
+    const unsigned bal = __ballot_sync(FULL, valid && fail);
+    if (lane == 0) A.bitmap[w] = bal;
   }
 }
 
