@@ -50,6 +50,8 @@ struct SampleLaunch {
 };
 
 __device__ __forceinline__ uint32_t ldn(const uint32_t* p, unsigned long long i) { return __ldg(p + i); }
+// 32-bit element offset from a list base: one IMAD.WIDE.U32 per address
+__device__ __forceinline__ uint32_t ldo(const uint32_t* p, uint32_t i) { return __ldg(p + i); }
 
 __device__ __forceinline__ VtxInfo load_vtx(const VtxInfo* vtx, uint32_t v) {
   const int4 raw = __ldg(reinterpret_cast<const int4*>(vtx + v));

@@ -42,6 +42,7 @@ namespace agpm_b200 {
 namespace {
 
 constexpr uint32_t INF = 0xffffffffu;
+constexpr unsigned long long kFrontierCap = 1ull << 23;  // samples per pass
 constexpr uint32_t NO_DRV = 0xffffffffu;
 
 // Per-sample intersection job; other-list slots are indexed by matching position.
@@ -86,7 +87,7 @@ struct FrontierArgs {
 __device__ __forceinline__ uint32_t lb_thread(const uint32_t* base, uint32_t lo, uint32_t hi, uint32_t x) {
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
-    if (ldn(base, mid) < x)
+    if (ldo(base, mid) < x)
       lo = mid + 1;
     else
       hi = mid;
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
     const IsectDesc<K>& d = desc[s];
     const uint32_t o = (uint32_t)(w - off[s]) * 32 + lane;
     const bool valid = o < d.dsize;
-    const uint32_t a = valid ? ldn(d.drv, o) : INF;
+    const uint32_t a = valid ? ldo(d.drv, o) : INF;
     bool fail = false;
 #pragma unroll
     for (int q = 0; q < K - 1; ++q) {
@@ -413,11 +414,11 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
         // a is inside [lo, hi) already, so membership in the restricted list is edge existence
         found = valid && edge_lookup(A.g.ehash, A.g.ehash_mask, a, d.owner[q]);
       } else if (nb <= 32) {
-        found = warp_contains((uint32_t)lane < nb ? ldn(B, lane) : INF, a);
+        found = warp_contains((uint32_t)lane < nb ? ldo(B, (uint32_t)lane) : INF, a);
       } else {
         // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then a short per-lane search
         const uint32_t step = nb / 33u;
-        const uint32_t sp = ldn(B, (uint32_t)(lane + 1) * step);
+        const uint32_t sp = ldo(B, (uint32_t)(lane + 1) * step);
         int c = 0;
 #pragma unroll
         for (int sh = 16; sh >= 1; sh >>= 1) {
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
         const uint32_t lo = c ? (uint32_t)c * step + 1 : 0;
         const uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step : nb;
         const uint32_t at = lb_thread(B, lo, hi, a);
-        found = at < nb && ldn(B, at) == a;
+        found = at < nb && ldo(B, at) == a;
       }
       fail = fail || (found == (bool)((d.outs >> q) & 1u));
     }
@@ -594,7 +595,7 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
     A.step_multi[st] = !(__builtin_popcount(in_m) == 1 && out_m == 0);
     A.step_reuse[st] = g_frontier_reuse && A.step_multi[st] && nests(L.p, st);
   }
-  const unsigned long long cap = std::min<unsigned long long>(L.count, 1ull << 22);
+  const unsigned long long cap = std::min<unsigned long long>(L.count, kFrontierCap);
   A.cap = cap;
   size_t bytes = 0;
   auto carve = [&](size_t n) {
