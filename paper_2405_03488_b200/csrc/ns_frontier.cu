@@ -42,7 +42,7 @@ namespace agpm_b200 {
 namespace {
 
 constexpr uint32_t INF = 0xffffffffu;
-constexpr unsigned long long kFrontierCap = 1ull << 23;  // samples per pass
+constexpr unsigned long long kFrontierCap = 1ull << 22;  // samples per pass
 constexpr uint32_t NO_DRV = 0xffffffffu;
 
 // Per-sample intersection job; other-list slots are indexed by matching position.
@@ -371,13 +371,8 @@ __device__ __forceinline__ bool warp_contains(uint32_t b, uint32_t a) {
   return __shfl_sync(FULL, b, pos) == a;
 }
 
-// One warp per pair of bitmap words (a word = 32 driver elements of ONE
-// sample); warps walk contiguous word runs so the owning samples are found once
-// (k-ary search over the word offsets) and then advanced. The kernel is bound
-// by the latency of a ~7-deep chain of dependent loads per word (descriptor,
-// driver, splitters, bucket probes), so two words are processed per iteration
-// with their chains interleaved — the bucket searches of both words run in one
-// fused branchless loop and their loads issue back to back.
+// One warp per bitmap word; warps walk contiguous word runs so the owning
+// sample is found once (k-ary over the word offsets) and then advanced.
 template <int K>
 __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, unsigned long long words) {
   const int lane = threadIdx.x & 31;
@@ -386,7 +381,7 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
   const uint32_t* __restrict__ nbr = A.g.nbr;
   const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
   const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-  const unsigned long long per = ((words + nwarps - 1) / nwarps + 1) & ~1ull;
+  const unsigned long long per = (words + nwarps - 1) / nwarps;
   const unsigned long long w0 = warp * per, w1 = min(words, w0 + per);
   if (w0 >= w1) return;
   unsigned long long s;
@@ -402,82 +397,44 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
     const unsigned long long pos = lo + lane;
     s = lo + __popc(__ballot_sync(FULL, pos < hi && off[pos] <= w0)) - 1;
   }
-  for (unsigned long long w = w0; w < w1; w += 2) {
-    const bool has_b = w + 1 < w1;
+  for (unsigned long long w = w0; w < w1; ++w) {
     while (off[s + 1] <= w) ++s;  // uniform
-    unsigned long long sb = s;
-    if (has_b)
-      while (off[sb + 1] <= w + 1) ++sb;
-    const IsectDesc<K>& dA = desc[s];
-    const IsectDesc<K>& dB = desc[sb];
-    const uint32_t oA = (uint32_t)(w - off[s]) * 32 + lane;
-    const uint32_t oB = (uint32_t)(w + 1 - off[sb]) * 32 + lane;
-    const bool vA = oA < dA.dsize, vB = has_b && oB < dB.dsize;
-    const uint32_t aA = vA ? ldo(dA.drv, oA) : INF, aB = vB ? ldo(dB.drv, oB) : INF;
-    const uint32_t listsA = dA.lists, listsB = has_b ? dB.lists : 0u;
-    const uint32_t outsA = dA.outs, outsB = dB.outs;
-    bool fA = false, fB = false;
+    const IsectDesc<K>& d = desc[s];
+    const uint32_t o = (uint32_t)(w - off[s]) * 32 + lane;
+    const bool valid = o < d.dsize;
+    const uint32_t a = valid ? ldo(d.drv, o) : INF;
+    bool fail = false;
 #pragma unroll
     for (int q = 0; q < K - 1; ++q) {
-      const bool actA = (listsA >> q) & 1u, actB = (listsB >> q) & 1u;
-      if (!actA && !actB) continue;  // uniform
-      const uint32_t* BA = nbr + (actA ? dA.start[q] : 0ull);
-      const uint32_t* BB = nbr + (actB ? dB.start[q] : 0ull);
-      const uint32_t nA = actA ? dA.len[q] : 0u, nB = actB ? dB.len[q] : 0u;
-      // splitters (lists <= 32: the list itself)
-      const uint32_t stA = nA <= 32 ? 0u : nA / 33u, stB = nB <= 32 ? 0u : nB / 33u;
-      const uint32_t spA = nA > 32 ? ldo(BA, (uint32_t)(lane + 1) * stA) : ((uint32_t)lane < nA ? ldo(BA, (uint32_t)lane) : INF);
-      const uint32_t spB = nB > 32 ? ldo(BB, (uint32_t)(lane + 1) * stB) : ((uint32_t)lane < nB ? ldo(BB, (uint32_t)lane) : INF);
-      int cA = 0, cB = 0;
+      if (!((d.lists >> q) & 1u)) continue;
+      bool found;
+      const uint32_t* B = nbr + d.start[q];
+      const uint32_t nb = d.len[q];
+      if (A.g.ehash) {
+        // a is inside [lo, hi) already, so membership in the restricted list is edge existence
+        found = valid && edge_lookup(A.g.ehash, A.g.ehash_mask, a, d.owner[q]);
+      } else if (nb <= 32) {
+        found = warp_contains((uint32_t)lane < nb ? ldo(B, (uint32_t)lane) : INF, a);
+      } else {
+        // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then a short per-lane search
+        const uint32_t step = nb / 33u;
+        const uint32_t sp = ldo(B, (uint32_t)(lane + 1) * step);
+        int c = 0;
 #pragma unroll
-      for (int sh = 16; sh >= 1; sh >>= 1) {
-        const uint32_t tA = __shfl_sync(FULL, spA, cA + sh - 1);
-        const uint32_t tB = __shfl_sync(FULL, spB, cB + sh - 1);
-        if (tA < aA) cA += sh;
-        if (tB < aB) cB += sh;
+        for (int sh = 16; sh >= 1; sh >>= 1) {
+          const uint32_t t = __shfl_sync(FULL, sp, c + sh - 1);
+          if (t < a) c += sh;
+        }
+        c += __shfl_sync(FULL, sp, c) < a ? 1 : 0;  // c = #splitters < a, in [0, 32]
+        const uint32_t lo = c ? (uint32_t)c * step + 1 : 0;
+        const uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step : nb;
+        const uint32_t at = lb_thread(B, lo, hi, a);
+        found = at < nb && ldo(B, at) == a;
       }
-      const uint32_t tcA = __shfl_sync(FULL, spA, cA), tcB = __shfl_sync(FULL, spB, cB);
-      bool foundA = tcA == aA, foundB = tcB == aB;
-      if (stA | stB) {  // some list needs a bucket search
-        cA += tcA < aA ? 1 : 0;
-        cB += tcB < aB ? 1 : 0;
-        uint32_t loA = cA ? (uint32_t)cA * stA + 1 : 0, loB = cB ? (uint32_t)cB * stB + 1 : 0;
-        uint32_t mA = stA ? (cA < 32 ? (uint32_t)(cA + 1) * stA : nA) - loA : 0u;
-        uint32_t mB = stB ? (cB < 32 ? (uint32_t)(cB + 1) * stB : nB) - loB : 0u;
-        while (mA > 1 || mB > 1) {  // fused branchless lower_bound over [lo, lo + m)
-          const uint32_t hA = mA >> 1, hB = mB >> 1;
-          const uint32_t xA = mA > 1 ? ldo(BA, loA + hA - 1) : INF;
-          const uint32_t xB = mB > 1 ? ldo(BB, loB + hB - 1) : INF;
-          if (mA > 1) {
-            loA = xA < aA ? loA + hA : loA;
-            mA -= hA;
-          }
-          if (mB > 1) {
-            loB = xB < aB ? loB + hB : loB;
-            mB -= hB;
-          }
-        }
-        // the answer is lo (+1 if one candidate is left and it is < a); an empty bucket
-        // (step == 1) still needs B[lo] itself
-        if (stA) {
-          const uint32_t yA = loA < nA ? ldo(BA, loA) : INF;
-          const uint32_t atA = loA + (mA == 1 && yA < aA ? 1u : 0u);
-          foundA = atA == loA ? yA == aA : (atA < nA && ldo(BA, atA) == aA);
-        }
-        if (stB) {
-          const uint32_t yB = loB < nB ? ldo(BB, loB) : INF;
-          const uint32_t atB = loB + (mB == 1 && yB < aB ? 1u : 0u);
-          foundB = atB == loB ? yB == aB : (atB < nB && ldo(BB, atB) == aB);
-        }
-      }
-      if (actA) fA = fA || (foundA == (bool)((outsA >> q) & 1u));
-      if (actB) fB = fB || (foundB == (bool)((outsB >> q) & 1u));
+      fail = fail || (found == (bool)((d.outs >> q) & 1u));
     }
-    const unsigned balA = __ballot_sync(FULL, vA && fA), balB = __ballot_sync(FULL, vB && fB);
-    if (lane == 0) {
-      A.bitmap[w] = balA;
-      if (has_b) A.bitmap[w + 1] = balB;
-    }
+    const unsigned bal = __ballot_sync(FULL, valid && fail);
+    if (lane == 0) A.bitmap[w] = bal;
   }
 }
 
@@ -695,7 +652,7 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
           A.survivors[slot] = static_cast<uint32_t*>(ctx.get(10 + slot, 4 * A.surv_cap + 64));
           AGPM_CUDA(cudaMemsetAsync(A.surv_cursor + slot, 0, 8, s));
         }
-        const unsigned long long warps = std::min<unsigned long long>((words + 1) / 2, (unsigned long long)sms * 64);
+        const unsigned long long warps = std::min<unsigned long long>(words, (unsigned long long)sms * 64);
         fr_isect_kernel<K><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(A, words);
         count_launch();
         AGPM_CUDA(cudaGetLastError());
