@@ -307,6 +307,33 @@ int agpm_calibrate_hardware_constant(double* out);
 int agpm_count_hybrid(const agpm_host_graph* hg, agpm_graph* g, const agpm_plan* plan, double eps, double confidence,
                       uint64_t seed, double profile_fraction, double hw_const, agpm_hybrid_result* out, void* stream);
 
+/* ---------------------------------------- dense/sparse region split -------
+ * Builder-defined (no reference implementation). On a
+ * degree-relabelled view: V_s = {deg < tau} = ids [0, tau_id); C_sparse =
+ * matches touching V_s, exact; C_dense on G[V_d] by dense_method 0 = online NS
+ * (eps, delta, max_samples), 1 = mean of `repeats` colourings with `colors`
+ * colours, 2 = exact. estimate = C_sparse + C_dense. */
+typedef struct agpm_region_result {
+  uint32_t tau_id;
+  uint32_t pad;
+  uint64_t sparse_vertices, dense_vertices, dense_edges;
+  int32_t rooted;      /* 1: C_sparse = root-restricted exact count; 0: exact(G) - exact(G[V_d]) */
+  int32_t dense_exact; /* 1: C_dense is exact (method 2 or an empty dense region) */
+  uint64_t c_sparse;
+  double c_dense, estimate, dense_epsilon_hat;
+  agpm_online_result dense_ns;
+  double sparse_seconds, dense_seconds;
+} agpm_region_result;
+
+/* exact count restricted to seeds whose first vertex is < root_limit */
+int agpm_exact_count_rooted(agpm_graph* g, const agpm_plan* plan, uint32_t root_limit, uint64_t* count,
+                            void* stream);
+/* subgraph induced on vertices >= min_vertex (ids unchanged) */
+int agpm_induced_suffix(agpm_graph* g, uint32_t min_vertex, agpm_graph** out, void* stream);
+int agpm_region_split(agpm_graph* g, const agpm_plan* plan, uint32_t tau_degree, int dense_method, double eps,
+                      double delta, uint64_t seed, uint32_t colors, uint32_t repeats, uint64_t max_samples,
+                      agpm_region_result* out, void* stream);
+
 /* ------------------------------------------------------- misc / device -----*/
 const char* agpm_last_error(void);
 int agpm_device_count(int* n);

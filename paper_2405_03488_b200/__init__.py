@@ -26,7 +26,7 @@ __all__ = [
     "lib", "compile_plan", "builtin_pattern_names", "automorphism_count", "scaling_rule_text",
     "plan_verifies_each_edge_once", "norm_cdf", "inv_norm_cdf", "predicted_error", "CsrGraph",
     "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
-    "hit_rate_report", "exact_count", "gs_estimate", "choose_keep_probability", "ns_cost_cone",
+    "hit_rate_report", "exact_count", "exact_count_rooted", "region_split", "gs_estimate", "choose_keep_probability", "ns_cost_cone",
     "gs_cost_estimate", "select_scheme", "count_matches_through_edge", "estimate_gamma", "fast_profile",
     "calibrate_hardware_constant", "count_hybrid", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
@@ -129,6 +129,10 @@ def _declare(L):
         "agpm_gs_estimate": (C.c_int, [A.P, A.pPlan, C.c_int, C.c_double, A.u32, A.u64, C.POINTER(A.GsResult), A.P]),
         "agpm_triangle_count": (C.c_int, [A.P, A.pu64, A.P]),
         "agpm_graph_max_degree": (C.c_int, [A.P, A.pu64]),
+        "agpm_exact_count_rooted": (C.c_int, [A.P, A.pPlan, A.u32, A.pu64, A.P]),
+        "agpm_induced_suffix": (C.c_int, [A.P, A.u32, C.POINTER(A.P), A.P]),
+        "agpm_region_split": (C.c_int, [A.P, A.pPlan, A.u32, C.c_int, C.c_double, C.c_double, A.u64, A.u32, A.u32,
+                                        A.u64, C.POINTER(A.RegionResult), A.P]),
         "agpm_choose_keep_probability": (C.c_int, [C.c_double] * 4 + [C.POINTER(A.KeepProbability)]),
         "agpm_ns_cost_cone": (C.c_int, [C.c_double, C.c_double, A.pPlan, A.u64, C.c_double, C.POINTER(A.CostCone)]),
         "agpm_gs_cost_estimate": (C.c_int, [C.c_double, C.c_double, A.pPlan, A.u32, C.c_double, A.u64,
@@ -374,6 +378,12 @@ class DeviceGraph:
         _check(lib().agpm_bernoulli_sparsify(self._h, keep_probability, seed, C.byref(h), stream))
         return DeviceGraph(_handle=h)
 
+    def induced_suffix(self, min_vertex, stream=None):
+        """Subgraph induced on vertices >= min_vertex (the dense region of a relabelled graph)."""
+        h = C.c_void_p()
+        _check(lib().agpm_induced_suffix(self._h, min_vertex, C.byref(h), stream))
+        return DeviceGraph(_handle=h)
+
     def triangle_count(self, stream=None):
         out = C.c_uint64()
         _check(lib().agpm_triangle_count(self._h, C.byref(out), stream))
@@ -430,6 +440,25 @@ def gs_estimate(dg, plan, scheme="color", keep_probability=1.0, colors=1, seed=0
     out = _abi.GsResult()
     _check(lib().agpm_gs_estimate(dg._h, C.byref(plan), {"bernoulli": 0, "color": 1}[scheme], keep_probability,
                                   colors, seed, C.byref(out), stream))
+    return out
+
+
+def exact_count_rooted(dg, plan, root_limit, stream=None):
+    out = C.c_uint64()
+    _check(lib().agpm_exact_count_rooted(dg._h, C.byref(plan), root_limit, C.byref(out), stream))
+    return out.value
+
+
+REGION_METHODS = {"ns": 0, "gs": 1, "exact": 2}
+
+
+def region_split(dg, plan, tau_degree, dense="ns", eps=0.01, delta=0.05, seed=1, colors=4, repeats=16,
+                 max_samples=1000000000, stream=None):
+    """Dense/sparse degree-threshold split (builder-defined):
+    exact count of matches touching {deg < tau} + an estimate on the dense region."""
+    out = _abi.RegionResult()
+    _check(lib().agpm_region_split(dg._h, C.byref(plan), tau_degree, REGION_METHODS[dense], eps, delta, seed, colors,
+                                   repeats, max_samples, C.byref(out), stream))
     return out
 
 

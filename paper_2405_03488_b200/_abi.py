@@ -142,6 +142,14 @@ class HybridResult(C.Structure):
                 ("gs", GsResult), ("ns", OnlineResult)]
 
 
+class RegionResult(C.Structure):
+    _fields_ = [("tau_id", C.c_uint32), ("pad", C.c_uint32), ("sparse_vertices", C.c_uint64),
+                ("dense_vertices", C.c_uint64), ("dense_edges", C.c_uint64), ("rooted", C.c_int32),
+                ("dense_exact", C.c_int32), ("c_sparse", C.c_uint64), ("c_dense", C.c_double),
+                ("estimate", C.c_double), ("dense_epsilon_hat", C.c_double), ("dense_ns", OnlineResult),
+                ("sparse_seconds", C.c_double), ("dense_seconds", C.c_double)]
+
+
 P = C.c_void_p
 u32, u64, i32, dbl = C.c_uint32, C.c_uint64, C.c_int, C.c_double
 pu32, pu64, pdbl, pu8 = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_uint8)

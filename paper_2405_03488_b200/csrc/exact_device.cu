@@ -74,7 +74,8 @@ __device__ __forceinline__ bool warp_member(const uint32_t* B, uint32_t nb, uint
 
 template <int K>
 __global__ void __launch_bounds__(256) exact_kernel(const GraphArgs g, const DevPlan p, const int apply_bounds,
-                                                    const int skip_unordered, uint32_t* __restrict__ scratch,
+                                                    const int skip_unordered, const uint32_t root_limit,
+                                                    uint32_t* __restrict__ scratch,
                                                     const uint32_t cap, unsigned long long* __restrict__ cursor,
                                                     unsigned long long* __restrict__ count_out) {
   constexpr int L = K - 2;  // steps
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const GraphArgs g, const Dev
     bnd[0] = (uint32_t)(arc >> 32);
     bnd[1] = (uint32_t)arc;
     if (skip_unordered && bnd[0] > bnd[1]) continue;  // exact_engine.cpp:84
+    if (bnd[0] >= root_limit) continue;                // region split: roots below the threshold only
     {
       const VtxInfo a = load_vtx(g.vtx, bnd[0]), b = load_vtx(g.vtx, bnd[1]);
       pb[0] = a.begin;
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const GraphArgs g, const Dev
 
 template <int K>
 unsigned long long run_exact_k(const agpm_graph* gr, const DevPlan& p, bool apply_bounds, bool skip_unordered,
-                               cudaStream_t s) {
+                               uint32_t root_limit, cudaStream_t s) {
   DeviceCtx& ctx = ctx_for_current_device();
   GraphArgs g{gr->vtx, gr->nbr, gr->seed_arcs, gr->arcs, gr->plain, nullptr, 0};
   int occ = 0;
@@ -255,8 +257,8 @@ unsigned long long run_exact_k(const agpm_graph* gr, const DevPlan& p, bool appl
   auto* scratch = static_cast<uint32_t*>(ctx.get(11, 4ull * warps * levels * cap + 64));
   auto* cnt = static_cast<unsigned long long*>(ctx.get(3, 64));
   AGPM_CUDA(cudaMemsetAsync(cnt, 0, 16, s));
-  exact_kernel<K><<<blocks, 256, 0, s>>>(g, p, apply_bounds ? 1 : 0, skip_unordered ? 1 : 0, scratch, cap, cnt,
-                                         cnt + 1);
+  exact_kernel<K><<<blocks, 256, 0, s>>>(g, p, apply_bounds ? 1 : 0, skip_unordered ? 1 : 0, root_limit, scratch,
+                                         cap, cnt, cnt + 1);
   count_launch();
   AGPM_CUDA(cudaGetLastError());
   unsigned long long h = 0;
@@ -267,8 +269,10 @@ unsigned long long run_exact_k(const agpm_graph* gr, const DevPlan& p, bool appl
 
 }  // namespace
 
-// exact_count (exact_engine.cpp:66-91), eager plans
-unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan, cudaStream_t s) {
+// exact_count (exact_engine.cpp:66-91), eager plans; root_limit keeps only
+// seeds whose first vertex is below it (region split)
+unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan, cudaStream_t s,
+                                      uint32_t root_limit) {
   if (!plan || plan->k < 2 || plan->k > AGPM_MAX_K || plan->n_steps != plan->k - 2)
     throw std::invalid_argument("malformed plan");
   const bool clique = plan->n_edges == plan->k * (plan->k - 1) / 2;
@@ -279,7 +283,8 @@ unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan
   const bool oriented_clique = g->oriented && clique;
   const bool apply_bounds = !oriented_clique;
   const bool skip_unordered = !oriented_clique && plan->seed_ordered;
-  if (plan->k == 2) return skip_unordered ? g->arcs / 2 : g->arcs;  // every (ordered) arc is a match
+  if (plan->k == 2 && root_limit == 0xffffffffu)
+    return skip_unordered ? g->arcs / 2 : g->arcs;  // every (ordered) arc is a match
   DevPlan d{};
   d.k = plan->k;
   d.n_steps = plan->n_steps;
@@ -298,13 +303,14 @@ unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan
   }
   if (g->arcs == 0) return 0;
   switch (plan->k) {
-    case 3: return run_exact_k<3>(g, d, apply_bounds, skip_unordered, s);
-    case 4: return run_exact_k<4>(g, d, apply_bounds, skip_unordered, s);
-    case 5: return run_exact_k<5>(g, d, apply_bounds, skip_unordered, s);
-    case 6: return run_exact_k<6>(g, d, apply_bounds, skip_unordered, s);
-    case 7: return run_exact_k<7>(g, d, apply_bounds, skip_unordered, s);
-    case 8: return run_exact_k<8>(g, d, apply_bounds, skip_unordered, s);
-    case 9: return run_exact_k<9>(g, d, apply_bounds, skip_unordered, s);
+    case 3: return run_exact_k<3>(g, d, apply_bounds, skip_unordered, root_limit, s);
+    case 4: return run_exact_k<4>(g, d, apply_bounds, skip_unordered, root_limit, s);
+    case 5: return run_exact_k<5>(g, d, apply_bounds, skip_unordered, root_limit, s);
+    case 6: return run_exact_k<6>(g, d, apply_bounds, skip_unordered, root_limit, s);
+    case 7: return run_exact_k<7>(g, d, apply_bounds, skip_unordered, root_limit, s);
+    case 8: return run_exact_k<8>(g, d, apply_bounds, skip_unordered, root_limit, s);
+    case 9: return run_exact_k<9>(g, d, apply_bounds, skip_unordered, root_limit, s);
+    case 2: throw std::invalid_argument("rooted counts of a single edge are not supported");
     default: throw std::invalid_argument("device exact counter needs 2 <= k <= 9");
   }
 }
@@ -314,6 +320,14 @@ unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan
 extern "C" int agpm_exact_count(agpm_graph* g, const agpm_plan* plan, uint64_t* count, void* stream) {
   return agpm_b200::guarded([&] {
     if (!g || !count) throw std::invalid_argument("null argument");
-    *count = agpm_b200::exact_count_device(g, plan, agpm_b200::pick_stream(stream));
+    *count = agpm_b200::exact_count_device(g, plan, agpm_b200::pick_stream(stream), 0xffffffffu);
+  });
+}
+
+extern "C" int agpm_exact_count_rooted(agpm_graph* g, const agpm_plan* plan, uint32_t root_limit, uint64_t* count,
+                                       void* stream) {
+  return agpm_b200::guarded([&] {
+    if (!g || !count) throw std::invalid_argument("null argument");
+    *count = agpm_b200::exact_count_device(g, plan, agpm_b200::pick_stream(stream), root_limit);
   });
 }
