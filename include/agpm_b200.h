@@ -312,7 +312,8 @@ int agpm_count_hybrid(const agpm_host_graph* hg, agpm_graph* g, const agpm_plan*
  * degree-relabelled view: V_s = {deg < tau} = ids [0, tau_id); C_sparse =
  * matches touching V_s, exact; C_dense on G[V_d] by dense_method 0 = online NS
  * (eps, delta, max_samples), 1 = mean of `repeats` colourings with `colors`
- * colours, 2 = exact. estimate = C_sparse + C_dense. */
+ * colours, 2 = exact. estimate = C_sparse + C_dense. On an oriented clique DAG
+ * tau_degree is taken as the id threshold tau_id itself. */
 typedef struct agpm_region_result {
   uint32_t tau_id;
   uint32_t pad;

@@ -183,8 +183,11 @@ int agpm_region_split(agpm_graph* g, const agpm_plan* plan, uint32_t tau_degree,
     unsigned long long h[2] = {0, 0};
     AGPM_CUDA(cudaMemcpyAsync(h, scratch, 16, cudaMemcpyDeviceToHost, s));
     AGPM_CUDA(cudaStreamSynchronize(s));
-    if (h[1]) throw std::invalid_argument("region split needs a degree-relabelled graph (degrees ascending with id)");
-    const uint32_t tau_id = static_cast<uint32_t>(h[0]);
+    // an oriented DAG's out-degrees are not the degrees the split is defined on:
+    // there `tau` is the id threshold itself (the symmetric view's tau_id)
+    if (!g->oriented && h[1])
+      throw std::invalid_argument("region split needs a degree-relabelled graph (degrees ascending with id)");
+    const uint32_t tau_id = g->oriented ? std::min(tau_degree, g->n) : static_cast<uint32_t>(h[0]);
     out->tau_id = tau_id;
     out->sparse_vertices = tau_id;
     out->dense_vertices = g->n - tau_id;

@@ -34,7 +34,7 @@ def test_oriented_clique_region(agpm):
     g = agpm.rmat(12, 16, seed=2).relabel_by_degree()
     plan = agpm.compile_plan("4clique")
     sym = agpm.region_split(agpm.DeviceGraph(g), plan, 30, dense="exact")
-    ori = agpm.region_split(agpm.DeviceGraph(g.orient_by_degree()), plan, 30, dense="exact")
+    ori = agpm.region_split(agpm.DeviceGraph(g.orient_by_degree()), plan, sym.tau_id, dense="exact")
     assert ori.rooted and sym.rooted
     assert (ori.c_sparse, ori.c_dense) == (sym.c_sparse, sym.c_dense)
 
