@@ -1,0 +1,60 @@
+"""GPU: BASELINE.json configs at their full sizes.
+
+config 1  triangle, er_graph(10^4, 20/9999, 1) relabelled: 2^20 samples seed 1
+          (fixed budget) and the exact count, against the oracle.
+config 2  4-clique, RMAT-20 ef16 relabelled, run_ns_online to 1 %@95 %: the device
+          run stops at the same n with the same hits as the oracle's own online run
+          (the C restatement, ~0.5 M samples), and the estimate is within the bound
+          of the exact count.
+config 4  needle: ER n = 2^22, avg degree 8, 1000 planted 5-cliques — the
+          region split finds every planted clique exactly.
+(config 3 / 5 sizes are exercised by bench.py and the parity suites at smaller
+scale; their exact counts are infeasible for the CPU oracle.)
+"""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config1(agpm, oracle):
+    g = agpm.er_graph(10000, 20 / 9999, 1).relabel_by_degree()
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan("triangle")
+    dg = agpm.DeviceGraph(g)
+    exact = agpm.exact_count(dg, plan)
+    assert exact == oracle.exact_count(off, nbr, g.edge_count, plan) == 1380  # SURVEY §6 probe
+    acc = agpm.run_fixed_budget(dg, plan, 1 << 20, 1)
+    o = oracle.fixed_budget(off, nbr, g.edge_count, plan, 1 << 20, 1)
+    assert acc.n == o.n == 1 << 20 and acc.hits == o.hits
+    assert abs(acc.sum - o.sum) <= 1e-12 * o.sum
+    assert abs(acc.sum / acc.n - exact) < 0.05 * exact
+
+
+@pytest.mark.slow
+def test_config2_online_parity(agpm, oracle):
+    g = agpm.rmat(20, 16, 0.57, 0.19, 0.19, seed=1).relabel_by_degree()
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan("4clique")
+    dg = agpm.DeviceGraph(g)
+    r = agpm.run_ns_online(dg, plan, 0.01, 0.05, agpm.OnlinePolicy(), seed=1)
+    o = oracle.ns_online(off, nbr, g.edge_count, plan, 0.01, 0.05, agpm.OnlinePolicy(), 1)
+    assert r.report.converged and o.report.converged
+    assert r.report.n == o.report.n and r.windows == o.windows and r.accumulator.hits == o.accumulator.hits
+    assert abs(r.report.mu - o.report.mu) <= 1e-12 * o.report.mu
+    # the exact 4-clique count on the oriented DAG (device) and the 1 %@95 % promise
+    exact = agpm.exact_count(agpm.DeviceGraph(g.orient_by_degree()), plan)
+    assert abs(r.report.mu - exact) <= 0.02 * exact
+
+
+@pytest.mark.slow
+def test_config4_needle(agpm):
+    n = 1 << 22
+    g = agpm.er_fast(n, n * 4, seed=4, planted_k=5, planted_count=1000).relabel_by_degree()
+    dg = agpm.DeviceGraph(g)
+    plan = agpm.compile_plan("5clique")
+    exact = agpm.exact_count(dg, plan)
+    assert exact >= 1000
+    res = agpm.region_split(dg, plan, 16, dense="gs", colors=4, repeats=8)
+    assert res.c_sparse + (int(res.c_dense) if res.dense_exact else 0) <= exact
+    full = agpm.region_split(dg, plan, 16, dense="exact")
+    assert full.estimate == exact
