@@ -27,6 +27,11 @@ struct __align__(16) VtxInfo {
 };
 
 void cuda_check(cudaError_t e, const char* what);
+
+// Every device neighbour array is followed by kNbrPad zeroed u32 so vector
+// loads of a 16-B-aligned window around any list position stay in bounds.
+constexpr uint64_t kNbrPad = 16;
+uint32_t* alloc_nbr(uint64_t len, cudaStream_t s);
 #define AGPM_CUDA(x) ::agpm_b200::cuda_check((x), #x)
 
 struct DeviceCtx {

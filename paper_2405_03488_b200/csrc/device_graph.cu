@@ -39,6 +39,13 @@ void* DeviceCtx::get(int slot, size_t bytes) {
   return scratch[slot];
 }
 
+uint32_t* alloc_nbr(uint64_t len, cudaStream_t s) {
+  uint32_t* p = nullptr;
+  AGPM_CUDA(cudaMalloc(&p, 4ull * (len + kNbrPad)));
+  AGPM_CUDA(cudaMemsetAsync(p + len, 0, 4ull * kNbrPad, s));
+  return p;
+}
+
 void* DeviceCtx::get_pinned(int slot, size_t bytes) {
   if (pinned_bytes[slot] < bytes) {
     if (pinned[slot]) AGPM_CUDA(cudaFreeHost(pinned[slot]));
@@ -209,7 +216,7 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
       AGPM_CUDA(cudaMalloc(&d_end, sizeof(uint64_t) * (n ? n : 1)));
       AGPM_CUDA(cudaMemcpyAsync(d_end, end, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s));
     }
-    AGPM_CUDA(cudaMalloc(&g->nbr, sizeof(uint32_t) * (neighbor_len ? neighbor_len : 1)));
+    g->nbr = alloc_nbr(neighbor_len, s);
     if (neighbor_len)
       AGPM_CUDA(cudaMemcpyAsync(g->nbr, neighbors, sizeof(uint32_t) * neighbor_len,
                                 cudaMemcpyHostToDevice, s));

@@ -138,7 +138,7 @@ agpm_graph* induced_suffix_device(const agpm_graph* g, uint32_t lo, cudaStream_t
   out->edge_count = g->oriented ? kept : kept / 2;
   out->nbr_len = kept;
   out->plain = true;
-  AGPM_CUDA(cudaMalloc(&out->nbr, 4ull * (kept ? kept : 1)));
+  out->nbr = alloc_nbr(kept, s);
   if (n) {
     induced_fill_kernel<<<grid(n), 256, 0, s>>>(g->vtx, g->nbr, n, lo, offs, out->nbr);
     count_launch();

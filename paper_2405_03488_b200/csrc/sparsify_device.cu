@@ -130,7 +130,7 @@ agpm_graph* color_split_device(const agpm_graph* g, uint32_t c, uint64_t seed, u
   AGPM_CUDA(cudaMalloc(&colors, 4ull * (n ? n : 1)));
   AGPM_CUDA(cudaMalloc(&begin, 8ull * (n ? n : 1)));
   AGPM_CUDA(cudaMalloc(&split, 8ull * (n ? n : 1)));
-  AGPM_CUDA(cudaMalloc(&out->nbr, 4ull * (g->nbr_len ? g->nbr_len : 1)));
+  out->nbr = alloc_nbr(g->nbr_len, s);
   auto* tot = static_cast<unsigned long long*>(ctx.get(3, 64));
   AGPM_CUDA(cudaMemsetAsync(tot, 0, 8, s));
   if (n) {
@@ -177,7 +177,7 @@ agpm_graph* bernoulli_device(const agpm_graph* g, double p, uint64_t seed, cudaS
   out->edge_count = kept / 2;  // csr_graph.cpp:211
   out->nbr_len = kept;
   out->plain = true;
-  AGPM_CUDA(cudaMalloc(&out->nbr, 4ull * (kept ? kept : 1)));
+  out->nbr = alloc_nbr(kept, s);
   if (n) {
     bern_fill_kernel<<<grid_for(n), 256, 0, s>>>(g->vtx, g->nbr, n, seed, p, offs, out->nbr);
     count_launch();
