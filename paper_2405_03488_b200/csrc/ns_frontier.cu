@@ -416,8 +416,7 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
       } else if (nb <= 32) {
         found = warp_contains((uint32_t)lane < nb ? ldo(B, (uint32_t)lane) : INF, a);
       } else {
-        // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then the bucket
-        // itself in ONE round of independent 16-B loads (no dependent probe chain)
+        // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then a short per-lane search
         const uint32_t step = nb / 33u;
         const uint32_t sp = ldo(B, (uint32_t)(lane + 1) * step);
         int c = 0;
@@ -427,24 +426,10 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
           if (t < a) c += sh;
         }
         c += __shfl_sync(FULL, sp, c) < a ? 1 : 0;  // c = #splitters < a, in [0, 32]
-        uint32_t lo = c ? (uint32_t)c * step + 1 : 0;
-        uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step : nb;  // lower_bound(a) in [lo, hi]
-        while (hi - lo >= 8) {  // only for lists > 297 elements
-          const uint32_t mid = (lo + hi) >> 1;
-          if (ldo(B, mid) < a) lo = mid + 1; else hi = mid;
-        }
-        // a, if present, sits in [lo, min(hi, nb - 1)] (<= 8 elements): scan an aligned 12-element window
-        const unsigned long long abs_lo = d.start[q] + lo;
-        const unsigned long long al = abs_lo & ~3ull;
-        const uint4* w4 = reinterpret_cast<const uint4*>(nbr + al);
-        const uint4 x0 = __ldg(w4), x1 = __ldg(w4 + 1), x2 = __ldg(w4 + 2);
-        const uint32_t hib = min(hi, nb - 1);                 // last list index that can hold a
-        const uint32_t first = (uint32_t)(abs_lo - al);       // window index of lo
-        const uint32_t last = lo <= hib ? first + (hib - lo) : 0;  // empty bucket: no window slot
-        const uint32_t xs[12] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y, x2.z, x2.w};
-        found = false;
-#pragma unroll
-        for (uint32_t t = 0; t < 12; ++t) found = found || (lo <= hib && t >= first && t <= last && xs[t] == a);
+        const uint32_t lo = c ? (uint32_t)c * step + 1 : 0;
+        const uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step : nb;
+        const uint32_t at = lb_thread(B, lo, hi, a);
+        found = at < nb && ldo(B, at) == a;
       }
       fail = fail || (found == (bool)((d.outs >> q) & 1u));
     }
