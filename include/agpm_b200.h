@@ -162,6 +162,25 @@ int agpm_graph_neighbor_len(const agpm_graph* g, uint64_t* len);
 /* copy the view back to host (tests): begin[n], end[n], neighbors[neighbor_len] */
 int agpm_graph_download(const agpm_graph* g, uint64_t* begin, uint64_t* end, uint32_t* neighbors);
 
+/* --------------------------------------------- device graph ingest -----
+ * The host builders above, run in HBM (radix sort / unique / relabel / CSR on
+ * the GPU); results are bit-identical to building on the host and uploading.
+ * relabel != 0 applies relabel_by_degree (rank of (degree, id)) on the way.
+ *   agpm_graph_from_edges_device  CsrGraph::from_edges (csr_graph.cpp:46-72);
+ *                                 pairs = host u32[2*count] (u0,v0,u1,v1,...)
+ *   agpm_gen_rmat_device          == agpm_gen_rmat (+relabel) on the device
+ *   agpm_gen_er_fast_device       == agpm_gen_er_fast (+relabel)
+ *   agpm_graph_relabel_device     == agpm_host_graph_relabel_by_degree
+ *   agpm_graph_orient_device      orient_by_degree (csr_graph.cpp:172) */
+int agpm_graph_from_edges_device(const uint32_t* pairs, uint64_t count, uint32_t min_vertex_count,
+                                 int relabel, void* stream, agpm_graph** out);
+int agpm_gen_rmat_device(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                         uint64_t seed, int relabel, void* stream, agpm_graph** out);
+int agpm_gen_er_fast_device(uint32_t n, uint64_t target_edges, uint64_t seed, uint32_t planted_k,
+                            uint32_t planted_count, int relabel, void* stream, agpm_graph** out);
+int agpm_graph_relabel_device(const agpm_graph* g, void* stream, agpm_graph** out);
+int agpm_graph_orient_device(const agpm_graph* g, void* stream, agpm_graph** out);
+
 /* ------------------------------------------------- neighbour sampling -----
  * Global sample id i uses CounterRng(seed, 0, i) (rng.hpp:26-56), i.e. the
  * reference's workers=1 streams (ns_engine.cpp:72): GPU results are

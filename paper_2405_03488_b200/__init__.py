@@ -115,6 +115,12 @@ def _declare(L):
         "agpm_graph_info": (C.c_int, [A.P, A.pu32, A.pu64, A.pu64, C.POINTER(C.c_int), A.pu64]),
         "agpm_graph_download": (C.c_int, [A.P, A.pu64, A.pu64, A.pu32]),
         "agpm_graph_neighbor_len": (C.c_int, [A.P, A.pu64]),
+        "agpm_graph_from_edges_device": (C.c_int, [A.pu32, A.u64, A.u32, C.c_int, A.P, C.POINTER(A.P)]),
+        "agpm_gen_rmat_device": (C.c_int, [A.u32, A.u32, C.c_double, C.c_double, C.c_double, A.u64, C.c_int, A.P,
+                                           C.POINTER(A.P)]),
+        "agpm_gen_er_fast_device": (C.c_int, [A.u32, A.u64, A.u64, A.u32, A.u32, C.c_int, A.P, C.POINTER(A.P)]),
+        "agpm_graph_relabel_device": (C.c_int, [A.P, A.P, C.POINTER(A.P)]),
+        "agpm_graph_orient_device": (C.c_int, [A.P, A.P, C.POINTER(A.P)]),
         "agpm_ns_draw": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pdbl, A.pu8, A.pu32, A.P]),
         "agpm_ns_fixed_budget": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.pAcc, A.P]),
         "agpm_ns_online": (C.c_int, [A.P, A.pPlan, C.c_double, C.c_double, C.POINTER(OnlinePolicy), A.u64,
@@ -327,6 +333,30 @@ def rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1):
 
 
 # ------------------------------------------------------------------ device graphs
+def _device_make(fn, *args):
+    h = C.c_void_p()
+    _check(fn(*args, C.byref(h)))
+    return DeviceGraph(_handle=h)
+
+
+def rmat_device(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, relabel=True, stream=None):
+    """rmat(...)[.relabel_by_degree()] built in HBM (agpm_gen_rmat_device)."""
+    return _device_make(lib().agpm_gen_rmat_device, scale, edge_factor, a, b, c, seed, int(relabel), stream)
+
+
+def er_fast_device(n, target_edges, seed, planted_k=0, planted_count=0, relabel=True, stream=None):
+    """er_fast(...)[.relabel_by_degree()] built in HBM (agpm_gen_er_fast_device)."""
+    return _device_make(lib().agpm_gen_er_fast_device, n, target_edges, seed, planted_k, planted_count,
+                        int(relabel), stream)
+
+
+def graph_from_edges_device(pairs, min_vertex_count=0, relabel=False, stream=None):
+    """CsrGraph::from_edges (csr_graph.cpp:46-72) built in HBM; pairs = (m, 2) ints."""
+    p = np.ascontiguousarray(np.asarray(pairs, dtype=np.uint32).reshape(-1, 2))
+    return _device_make(lib().agpm_graph_from_edges_device, _ptr(p, C.c_uint32), len(p), min_vertex_count,
+                        int(relabel), stream)
+
+
 class DeviceGraph:
     """Device-resident CsrView mirror (agpm_graph)."""
 
@@ -352,6 +382,14 @@ class DeviceGraph:
         if h and h.value and _lib is not None:
             _lib.agpm_graph_free(h)
             self._h = None
+
+    def relabel_by_degree(self, stream=None):
+        """relabel_by_degree on the device (plain undirected views)."""
+        return _device_make(lib().agpm_graph_relabel_device, self._h, stream)
+
+    def orient_by_degree(self, stream=None):
+        """orient_by_degree (csr_graph.cpp:172) on the device."""
+        return _device_make(lib().agpm_graph_orient_device, self._h, stream)
 
     def download(self):
         """(begin u64[n], end u64[n], neighbors u32[neighbor_len]) of the view (tests)."""
@@ -392,8 +430,10 @@ class DeviceGraph:
     def info(self):
         n, m, arcs, o, by = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_int(), C.c_uint64()
         _check(lib().agpm_graph_info(self._h, C.byref(n), C.byref(m), C.byref(arcs), C.byref(o), C.byref(by)))
+        md = C.c_uint64()
+        _check(lib().agpm_graph_max_degree(self._h, C.byref(md)))
         return {"vertex_count": n.value, "edge_count": m.value, "arcs": arcs.value, "oriented": bool(o.value),
-                "device_bytes": by.value}
+                "device_bytes": by.value, "max_degree": md.value}
 
 
 def draw_samples(dg, plan, seed, first_id, count, with_bindings=True, stream=None):
@@ -557,6 +597,11 @@ def set_frontier_reuse(on):
 
 def kernel_launches():
     return lib().agpm_kernel_launches()
+
+
+def sync(stream=None):
+    """Wait for the library stream (or `stream`)."""
+    _check(lib().agpm_sync(stream))
 
 
 def device_count():
