@@ -1,4 +1,4 @@
-// Shared pieces of the two sampling kernels (ns_lane.cu, ns_warp.cu).
+// Shared pieces of the sampling kernels (ns_lane.cu, ns_warp.cu, ns_frontier.cu, ns_lazy.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -27,6 +27,13 @@ struct DevPlan {
   unsigned short out_mask[AGPM_MAX_K - 2];
   unsigned short gt_mask[AGPM_MAX_K - 2];
   unsigned short lt_mask[AGPM_MAX_K - 2];
+  // lazy verification (VerifyMode::Lazy, walker.hpp:56-62 / 88-107), positions
+  int lazy;
+  unsigned char tree_parent[AGPM_MAX_K - 2];
+  unsigned char n_closure, n_terminal, n_nonadj;
+  unsigned char closure[AGPM_MAX_PAIRS][2];   // edges not checked by a tree parent
+  unsigned char terminal[AGPM_MAX_PAIRS][2];  // binding[a] < binding[b]
+  unsigned char nonadj[AGPM_MAX_PAIRS][2];    // induced: must NOT be adjacent
 };
 
 struct GraphArgs {
@@ -75,6 +82,64 @@ __device__ __forceinline__ unsigned long long lower_bound_dev(const uint32_t* nb
   return lo;
 }
 
+constexpr uint32_t kNoVertex = 0xffffffffu;
+
+// lower_bound of x within base[lo, hi] (answer in [lo, hi]); warp-uniform
+// arguments, result uniform. `found` = (answer < hi && base[answer] == x).
+__device__ __forceinline__ uint32_t kary_lb(const uint32_t* base, uint32_t lo, uint32_t hi, uint32_t x,
+                                            int lane, bool* found) {
+  const uint32_t end = hi;
+  while (hi - lo > 32) {
+    // 32 probes at lo + (i+1)*step, step = floor(span/33) >= 1, all < hi
+    const uint32_t step = (hi - lo) / 33u;
+    const unsigned bal = __ballot_sync(FULL, ldn(base, lo + (uint32_t)(lane + 1) * step) < x);
+    const uint32_t c = __popc(bal);
+    const uint32_t nlo = c ? lo + c * step + 1 : lo;
+    hi = c < 32 ? lo + (c + 1) * step : hi;
+    lo = nlo;
+  }
+  const uint32_t n = hi - lo;
+  const uint32_t v = (uint32_t)lane < n ? ldn(base, lo + lane) : kNoVertex;
+  const uint32_t r = lo + __popc(__ballot_sync(FULL, v < x));
+  if (found) *found = r < end && ldn(base, r) == x;  // the answer may sit just past the last window
+  return r;
+}
+
+// per-lane branchless lower_bound of a in base[0, n): the trip count depends
+// only on n (warp-uniform), so lanes never diverge
+__device__ __forceinline__ uint32_t lane_lb(const uint32_t* base, uint32_t n, uint32_t a) {
+  if (n == 0) return 0;
+  uint32_t b = 0;
+  while (n > 1) {
+    const uint32_t half = n >> 1;
+    b = ldn(base, b + half - 1) < a ? b + half : b;
+    n -= half;
+  }
+  return b + (ldn(base, b) < a ? 1u : 0u);
+}
+
+// b ascending across lanes (kNoVertex padded); does any lane hold a?
+__device__ __forceinline__ bool chunk_contains(uint32_t b, uint32_t a) {
+  int pos = 0;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t t = __shfl_sync(FULL, b, pos + s - 1);
+    if (t < a) pos += s;
+  }
+  return __shfl_sync(FULL, b, pos) == a;
+}
+
+// number of lanes whose b (ascending across lanes, kNoVertex padded) is < a
+__device__ __forceinline__ uint32_t chunk_rank(uint32_t b, uint32_t a) {
+  int pos = 0;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t t = __shfl_sync(FULL, b, pos + s - 1);
+    if (t < a) pos += s;
+  }
+  return (uint32_t)pos + (__shfl_sync(FULL, b, pos) < a ? 1u : 0u);
+}
+
 // 32-B sector span of u32 elements [a, b) (B_min model)
 __device__ __forceinline__ unsigned long long sectors(unsigned long long a, unsigned long long b) {
   return b > a ? ((b * 4 - 1) >> 5) - ((a * 4) >> 5) + 1 : 0;
@@ -83,6 +148,7 @@ __device__ __forceinline__ unsigned long long sectors(unsigned long long a, unsi
 void launch_ns_lane(const SampleLaunch& L, cudaStream_t s);
 void launch_ns_warp(const SampleLaunch& L, cudaStream_t s);
 void launch_ns_frontier(const SampleLaunch& L, cudaStream_t s);
+void launch_ns_lazy(const SampleLaunch& L, cudaStream_t s);
 void set_frontier_reuse(bool on);
 
 }  // namespace agpm_b200

@@ -109,8 +109,7 @@ DevPlan make_dev_plan(const agpm_graph* g, const agpm_plan* plan) {
   if (!plan) throw std::invalid_argument("null plan");
   if (plan->k < 2 || plan->k > AGPM_MAX_K || plan->n_steps != plan->k - 2)
     throw std::invalid_argument("malformed plan");
-  if (plan->verify_mode != 0)
-    throw std::invalid_argument("the device sampler implements eager verification (VerifyMode::Eager)");
+  if (plan->verify_mode != 0 && plan->verify_mode != 1) throw std::invalid_argument("unknown verify mode");
   if (g->edge_count == 0) throw std::invalid_argument("cannot sample from an empty graph");
   if (g->oriented) throw std::invalid_argument("sampling runs on the symmetric graph");
   DevPlan d{};
@@ -131,6 +130,41 @@ DevPlan make_dev_plan(const agpm_graph* g, const agpm_plan* plan) {
     d.out_mask[s] = (unsigned short)out;
     d.gt_mask[s] = (unsigned short)gt;
     d.lt_mask[s] = (unsigned short)lt;
+    if (st.tree_parent < 0 || st.tree_parent >= s + 2) {
+      if (plan->verify_mode == 1) throw std::invalid_argument("malformed plan step");
+    } else {
+      d.tree_parent[s] = (unsigned char)st.tree_parent;
+    }
+  }
+  d.lazy = plan->verify_mode == 1;
+  if (d.lazy) {  // pattern vertices -> positions (walker.hpp:88-107)
+    auto pos = [&](int v) {
+      if (v < 0 || v >= plan->k) throw std::invalid_argument("malformed plan");
+      return (unsigned char)plan->pos_of[v];
+    };
+    if (plan->n_closure < 0 || plan->n_closure > AGPM_MAX_PAIRS || plan->n_terminal < 0 ||
+        plan->n_terminal > AGPM_MAX_PAIRS)
+      throw std::invalid_argument("malformed plan");
+    for (int i = 0; i < plan->n_closure; ++i) {
+      d.closure[i][0] = pos(plan->closure_edges[i][0]);
+      d.closure[i][1] = pos(plan->closure_edges[i][1]);
+    }
+    d.n_closure = (unsigned char)plan->n_closure;
+    for (int i = 0; i < plan->n_terminal; ++i) {
+      d.terminal[i][0] = pos(plan->terminal_constraints[i][0]);
+      d.terminal[i][1] = pos(plan->terminal_constraints[i][1]);
+    }
+    d.n_terminal = (unsigned char)plan->n_terminal;
+    int na = 0;
+    if (plan->induced)
+      for (int a = 0; a < plan->k; ++a)
+        for (int b = a + 1; b < plan->k; ++b)
+          if (!((plan->adjacency[a] >> b) & 1u)) {
+            d.nonadj[na][0] = pos(a);
+            d.nonadj[na][1] = pos(b);
+            ++na;
+          }
+    d.n_nonadj = (unsigned char)na;
   }
   return d;
 }
@@ -167,6 +201,12 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
   auto* cursor = static_cast<unsigned long long*>(ctx.get(0, 64));
   AGPM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
   if (dp.k < 3 || dp.k > AGPM_MAX_K) throw std::invalid_argument("device sampler needs 3 <= k <= 9");
+  if (dp.lazy) {  // NS-base: one warp per sample streams the union of the bound lists
+    if (d_bytes) throw std::invalid_argument("the B_min sector model is defined for eager plans");
+    SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, nullptr};
+    launch_ns_lazy(L, s);
+    return;
+  }
   const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, count);  // B_min replay: warp kernel
   // (the edge-hash membership path is available but off: on RMAT-20 it turned
   // L2-local list searches into random HBM sectors and ran 2.6x slower)

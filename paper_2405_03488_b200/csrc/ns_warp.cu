@@ -29,51 +29,6 @@ namespace {
 constexpr uint32_t INF = 0xffffffffu;
 constexpr int kWarpBatch = 8;  // sample ids claimed per cursor atomic
 
-// lower_bound of x within base[lo, hi] (answer in [lo, hi]); warp-uniform
-// arguments, result uniform. `found` = (answer < hi && base[answer] == x).
-__device__ __forceinline__ uint32_t kary_lb(const uint32_t* base, uint32_t lo, uint32_t hi, uint32_t x,
-                                            int lane, bool* found) {
-  const uint32_t end = hi;
-  while (hi - lo > 32) {
-    // 32 probes at lo + (i+1)*step, step = floor(span/33) >= 1, all < hi
-    const uint32_t step = (hi - lo) / 33u;
-    const unsigned bal = __ballot_sync(FULL, ldn(base, lo + (uint32_t)(lane + 1) * step) < x);
-    const uint32_t c = __popc(bal);
-    const uint32_t nlo = c ? lo + c * step + 1 : lo;
-    hi = c < 32 ? lo + (c + 1) * step : hi;
-    lo = nlo;
-  }
-  const uint32_t n = hi - lo;
-  const uint32_t v = (uint32_t)lane < n ? ldn(base, lo + lane) : INF;
-  const uint32_t r = lo + __popc(__ballot_sync(FULL, v < x));
-  if (found) *found = r < end && ldn(base, r) == x;  // the answer may sit just past the last window
-  return r;
-}
-
-// per-lane branchless lower_bound of a in base[0, n): the trip count depends
-// only on n (warp-uniform), so lanes never diverge
-__device__ __forceinline__ uint32_t lane_lb(const uint32_t* base, uint32_t n, uint32_t a) {
-  if (n == 0) return 0;
-  uint32_t b = 0;
-  while (n > 1) {
-    const uint32_t half = n >> 1;
-    b = ldn(base, b + half - 1) < a ? b + half : b;
-    n -= half;
-  }
-  return b + (ldn(base, b) < a ? 1u : 0u);
-}
-
-// b ascending across lanes (INF padded); does any lane hold a?
-__device__ __forceinline__ bool chunk_contains(uint32_t b, uint32_t a) {
-  int pos = 0;
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const uint32_t t = __shfl_sync(FULL, b, pos + s - 1);
-    if (t < a) pos += s;
-  }
-  return __shfl_sync(FULL, b, pos) == a;
-}
-
 template <int K, bool COUNT_BYTES>
 __global__ void __launch_bounds__(kThreads) ns_warp_kernel(const SampleLaunch L) {
   __shared__ uint32_t s_ballot[kWarps][kBallotWords];

@@ -48,9 +48,37 @@ BUILTINS = ["triangle", "4clique", "5clique", "6clique", "7clique", "8clique", "
 ER_SMALL = [(7, 0.45, 321), (9, 0.35, 101), (12, 0.3, 500), (60, 0.2, 17), (100, 0.1, 66), (200, 0.08, 71)]
 
 
+LAZY_CASES = [((200, 0.08, 71), "4clique", 9, 12345, 256), ((100, 0.1, 66), "triangle", 5, 0, 256),
+              ((60, 0.2, 17), "4cycle", 3, 77, 256), ((60, 0.2, 17), "house", 3, 0, 256),
+              ((60, 0.2, 17), "4motif-star", 8, 0, 256), ((100, 0.1, 66), "5path", 11, 500, 256),
+              ((200, 0.08, 71), "dumbbell", 2, 0, 128), ((60, 0.2, 17), "4motif-diamond", 4, 9, 256),
+              ((60, 0.2, 17), "5clique", 6, 0, 256)]
+
+
+def lazy_records(R):
+    """Lazy-verify (NS-base) draw records and online runs (ns_engine.cpp:27-53, 106-140)."""
+    out = {"records": {}, "online": {}}
+    for (n, p, seed_g), pat, seed, first, count in LAZY_CASES:
+        g = R.er_graph(n, p, seed_g)
+        v, h, b = R.draw_records(g, pat, seed, first, count, mode=1)
+        out["records"][f"er|{n}|{p!r}|{seed_g}|{pat}|{seed}|{first}"] = {
+            "values": [float(x).hex() for x in v], "hits": h.tolist(), "bindings": b.tolist()}
+    for (n, p, seed_g), pat, eps in [((200, 0.08, 71), "triangle", 0.05), ((200, 0.08, 71), "4cycle", 0.1)]:
+        g = R.er_graph(n, p, seed_g)
+        r = R.ns_online(g, pat, eps, 0.05, OnlinePolicy(1000, 10**7, 0), 3, mode=1)
+        out["online"][f"er|{n}|{p!r}|{seed_g}|{pat}|{eps!r}"] = {
+            "n": r.report.n, "windows": r.windows, "hits": r.accumulator.hits, "mu": float(r.report.mu).hex(),
+            "converged": r.report.converged}
+    dump("samples_lazy.json", out)
+
+
 def main():
     build_oracle(ref=True)
     R = RefLib()
+    if sys.argv[1:] == ["lazy"]:
+        lazy_records(R)
+        return
+    lazy_records(R)
 
     # ---------------------------------------------------------------- rng (rng.hpp)
     rng = {"derive_key": [], "u64": [], "below": [], "double": [], "edge_keep": [], "vertex_color": []}

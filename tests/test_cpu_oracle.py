@@ -78,6 +78,31 @@ def test_draw_records(agpm, oracle):
         assert b.tolist() == rec["bindings"], key
 
 
+def test_lazy_draw_records_and_online(agpm, oracle):
+    """Lazy verification (NS-base, walker.hpp:56-62 / 88-107): the oracle's records
+    and online stop points equal the compiled reference's (samples_lazy.json)."""
+    g = load("samples_lazy.json")
+    for key, rec in g["records"].items():
+        _, n, p, sg, pat, seed, first = key.split("|")
+        graph = _er(agpm, int(n), float(p), int(sg))
+        off, nbr = graph.arrays()
+        plan = agpm.compile_plan(pat, "lazy")
+        count = len(rec["values"])
+        v, h, b = oracle.draw_records(off, nbr, graph.edge_count, plan, int(seed), int(first), count)
+        assert [float(x).hex() for x in v] == rec["values"], key
+        assert h.tolist() == rec["hits"], key
+        assert b.tolist() == rec["bindings"], key
+    for key, rec in g["online"].items():
+        _, n, p, sg, pat, eps = key.split("|")
+        graph = _er(agpm, int(n), float(p), int(sg))
+        off, nbr = graph.arrays()
+        r = oracle.ns_online(off, nbr, graph.edge_count, agpm.compile_plan(pat, "lazy"), float(eps), 0.05,
+                             OnlinePolicy(1000, 10**7, 0), 3)
+        assert (r.report.n, r.windows, r.accumulator.hits, r.report.converged) == \
+            (rec["n"], rec["windows"], rec["hits"], rec["converged"]), key
+        assert float(r.report.mu).hex() == rec["mu"], key
+
+
 def test_config1_records_hash(agpm, oracle):
     """Config 1 (er_graph(10^4, 20/9999, 1), degree-relabelled), triangle, seed 1: the first
     2^16 sample records hash-equal the reference's."""
