@@ -222,6 +222,10 @@ int agpm_ns_set_strategy(int strategy);
 /* frontier only: let a step whose lists nest the previous step's (cliques)
  * intersect that step's survivors instead of recomputing (same samples). */
 int agpm_ns_set_frontier_reuse(int on);
+/* frontier only: dimension C of the dense-core adjacency bit matrix (top C ids,
+ * C*C/8 bytes, kept in L2) that answers core-core membership tests in one
+ * load; 0 disables; default 16384. Results are identical either way. */
+int agpm_ns_set_core_dim(uint32_t dim);
 
 /* Device-pointer building blocks (bench / multi-rank driver): enqueue only.
  * d_values: count f64 device buffer. */

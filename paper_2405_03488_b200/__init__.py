@@ -152,6 +152,7 @@ def _declare(L):
         "agpm_count_hybrid": (C.c_int, [A.P, A.P, A.pPlan, C.c_double, C.c_double, A.u64, C.c_double, C.c_double,
                                         C.POINTER(A.HybridResult), A.P]),
         "agpm_ns_set_frontier_reuse": (C.c_int, [C.c_int]),
+        "agpm_ns_set_core_dim": (C.c_int, [A.u32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -588,6 +589,11 @@ STRATEGIES = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3}
 def set_strategy(name):
     """Sampler kernel choice (all draw identical samples): auto | warp | lane | frontier."""
     _check(lib().agpm_ns_set_strategy(STRATEGIES[name]))
+
+
+def set_core_dim(dim):
+    """Dense-core bit-matrix dimension for the frontier sampler (0 = off, default 16384)."""
+    _check(lib().agpm_ns_set_core_dim(int(dim)))
 
 
 def set_frontier_reuse(on):

@@ -1,0 +1,94 @@
+// Dense-core adjacency bit matrix for the frontier intersections.
+//
+// On a degree-relabelled graph the highest ids are the highest-degree
+// vertices, and eager-verify candidates always sit above the bound vertices'
+// ids for clique-like steps — so most membership tests "a in N(w)" of the
+// intersection phase have both a and w among the top ids. For the top C ids
+// (the "core", default C = 16384 -> a 32 MB matrix that stays in the 126 MB L2)
+// the adjacency is kept as a C x C bit matrix: a core test is ONE L2 word load
+// per lane instead of a splitter load, a shuffle search and a dependent
+// per-lane search. Measured on config 2: 92 % of the isect membership tests
+// fall inside a 16 K core (tools: profiles/r1/README.md).
+//
+// Exact by construction (it is the adjacency restricted to [base, n)), so it
+// changes no result; it only replaces how membership is answered.
+#include <algorithm>
+
+#include "device.cuh"
+#include "ns_common.cuh"
+
+namespace agpm_b200 {
+namespace {
+
+uint32_t g_core_dim = 16384;
+
+// one warp per core row: build the row in shared memory, then write it out
+__global__ void __launch_bounds__(256) core_rows_kernel(const VtxInfo* __restrict__ vtx,
+                                                        const uint32_t* __restrict__ nbr, uint32_t base,
+                                                        uint32_t rows, uint32_t wpr, uint32_t* __restrict__ bits) {
+  extern __shared__ uint32_t sh[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  uint32_t* row = sh + (size_t)wib * wpr;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+    for (uint32_t i = lane; i < wpr; i += 32) row[i] = 0;
+    __syncwarp();
+    const VtxInfo vi = load_vtx(vtx, base + r);
+    const uint32_t* list = nbr + vi.begin;
+    const uint32_t start = kary_lb(list, 0, vi.deg, base, lane, nullptr);
+    for (uint32_t i = start + lane; i < vi.deg; i += 32) {
+      const uint32_t c = __ldg(list + i) - base;
+      atomicOr(row + (c >> 5), 1u << (c & 31));
+    }
+    __syncwarp();
+    uint32_t* out = bits + (unsigned long long)r * wpr;
+    for (uint32_t i = lane; i < wpr; i += 32) out[i] = row[i];
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+void set_core_dim(uint32_t dim) { g_core_dim = dim; }
+
+void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
+  const uint32_t want = g->oriented || !g->plain ? 0u : std::min(g_core_dim, g->n);
+  if (g->core && g->core_dim == want) return;
+  if (g->core) {
+    AGPM_CUDA(cudaStreamSynchronize(s));
+    AGPM_CUDA(cudaFree(g->core));
+    g->bytes -= 4ull * g->core_wpr * g->core_dim;
+    g->core = nullptr;
+    g->core_dim = g->core_wpr = g->core_base = 0;
+  }
+  if (want == 0) return;
+  DeviceCtx& ctx = ctx_for_current_device();
+  const uint32_t base = g->n - want;
+  const uint32_t wpr = (want + 31) / 32;
+  uint32_t* bits = nullptr;
+  AGPM_CUDA(cudaMalloc(&bits, 4ull * wpr * want));
+  const size_t shmem = 8ull * 4 * wpr;
+  if (shmem > 48 * 1024)
+    AGPM_CUDA(cudaFuncSetAttribute(core_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+  const unsigned blocks = std::max(1u, std::min((want + 7) / 8, (unsigned)ctx.sm_count * 4));
+  core_rows_kernel<<<blocks, 256, shmem, s>>>(g->vtx, g->nbr, base, want, wpr, bits);
+  count_launch();
+  AGPM_CUDA(cudaGetLastError());
+  g->core = bits;
+  g->core_base = base;
+  g->core_wpr = wpr;
+  g->core_dim = want;
+  g->bytes += 4ull * wpr * want;
+}
+
+}  // namespace agpm_b200
+
+using namespace agpm_b200;
+
+extern "C" int agpm_ns_set_core_dim(uint32_t dim) {
+  return guarded([&] {
+    if (dim > 65536) throw std::invalid_argument("core dimension must be <= 65536");
+    set_core_dim(dim);
+  });
+}

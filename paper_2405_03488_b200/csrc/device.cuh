@@ -68,6 +68,8 @@ struct agpm_graph {
   unsigned long long* seed_arcs = nullptr;
   unsigned long long* ehash = nullptr;  // edge-membership table (edge_hash.cuh), built on demand
   uint32_t ehash_mask = 0;
+  uint32_t* core = nullptr;  // dense-core bit matrix (core_bits.cu), built on demand
+  uint32_t core_base = 0, core_wpr = 0, core_dim = 0;
   uint64_t bytes = 0;
 };
 
@@ -79,4 +81,6 @@ void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsig
                    cudaStream_t s);
 // build g->ehash if absent (symmetric or oriented views alike: keys are unordered pairs)
 void ensure_edge_hash(agpm_graph* g, cudaStream_t s);
+// build (or drop, when the configured dimension is 0) g->core for the current core dimension
+void ensure_core_bits(agpm_graph* g, cudaStream_t s);
 }  // namespace agpm_b200

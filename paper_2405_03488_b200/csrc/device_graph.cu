@@ -234,6 +234,7 @@ int agpm_graph_free(agpm_graph* g) {
     cudaFree(g->nbr);
     cudaFree(g->seed_arcs);
     if (g->ehash) cudaFree(g->ehash);
+    if (g->core) cudaFree(g->core);
     delete g;
   });
 }

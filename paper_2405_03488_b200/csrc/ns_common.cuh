@@ -44,7 +44,18 @@ struct GraphArgs {
   int plain;
   const unsigned long long* __restrict__ ehash;  // edge table (frontier sampler)
   uint32_t ehash_mask;
+  // dense-core adjacency bit matrix (core_bits.cu): bit (u - core_base, v - core_base)
+  // of row-major rows of core_wpr words, for u, v >= core_base; null = off
+  const uint32_t* __restrict__ core;
+  uint32_t core_base;
+  uint32_t core_wpr;
 };
+
+// u, v >= core_base required
+__device__ __forceinline__ bool core_has_edge(const GraphArgs& g, uint32_t u, uint32_t v) {
+  const uint32_t c = v - g.core_base;
+  return (__ldg(g.core + (unsigned long long)(u - g.core_base) * g.core_wpr + (c >> 5)) >> (c & 31)) & 1u;
+}
 
 struct SampleLaunch {
   GraphArgs g;

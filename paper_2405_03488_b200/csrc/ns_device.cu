@@ -178,6 +178,9 @@ GraphArgs graph_args(const agpm_graph* g) {
   a.plain = g->plain;
   a.ehash = nullptr;  // see enqueue_sample
   a.ehash_mask = 0;
+  a.core = g->core;
+  a.core_base = g->core_base;
+  a.core_wpr = g->core_wpr;
   return a;
 }
 
@@ -208,6 +211,7 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
     return;
   }
   const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, count);  // B_min replay: warp kernel
+  if (strat == kStrategyFrontier) ensure_core_bits(const_cast<agpm_graph*>(g), s);
   // (the edge-hash membership path is available but off: on RMAT-20 it turned
   // L2-local list searches into random HBM sectors and ran 2.6x slower)
   SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};

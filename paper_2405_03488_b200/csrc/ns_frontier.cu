@@ -57,6 +57,7 @@ struct __align__(16) IsectDesc {
   uint32_t outs;                      // bit q: ... and an out-list (difference)
   uint32_t drv_pos;                   // position owning the driver list, NO_DRV for survivors
   uint32_t drv_rs;                    // driver range start relative to that list
+  uint32_t core;                      // bit q: list q is answered by the dense-core bit matrix
 };
 
 struct FrontierArgs {
@@ -304,7 +305,10 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
     IsectDesc<K> d;
     d.drv = dptr;
     d.dsize = dsize;
-    d.lists = d.outs = 0;
+    d.lists = d.outs = d.core = 0;
+    // every driver element is >= lo: with lo inside the core, a list whose owner
+    // is a core vertex is answered by one bit of the core matrix
+    const bool drv_in_core = A.g.core && lo >= A.g.core_base;
 #pragma unroll
     for (int q = 0; q < K - 1; ++q) {
       d.start[q] = 0;
@@ -316,6 +320,7 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
         d.len[q] = is_out ? S.pd[q] : re[q] - rs[q];
         d.lists |= 1u << q;
         if (is_out) d.outs |= 1u << q;
+        if (drv_in_core && S.bnd[q] >= A.g.core_base) d.core |= 1u << q;
       }
     }
     d.drv_pos = reuse ? NO_DRV : (uint32_t)drv;
@@ -371,8 +376,11 @@ __device__ __forceinline__ bool warp_contains(uint32_t b, uint32_t a) {
   return __shfl_sync(FULL, b, pos) == a;
 }
 
-// One warp per bitmap word; warps walk contiguous word runs so the owning
-// sample is found once (k-ary over the word offsets) and then advanced.
+// One warp per bitmap word; each warp walks a contiguous run of words. The run
+// is consumed sample by sample: the owning sample is located once (k-ary over
+// the word offsets, then 32 offsets per probe), its descriptor is read once
+// into registers, and its words follow. Core lists cost one L2 word per lane;
+// the rest load 32 splitters and finish with a short per-lane search.
 template <int K>
 __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, unsigned long long words) {
   const int lane = threadIdx.x & 31;
@@ -397,44 +405,58 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
     const unsigned long long pos = lo + lane;
     s = lo + __popc(__ballot_sync(FULL, pos < hi && off[pos] <= w0)) - 1;
   }
-  for (unsigned long long w = w0; w < w1; ++w) {
-    while (off[s + 1] <= w) ++s;  // uniform
-    const IsectDesc<K>& d = desc[s];
-    const uint32_t o = (uint32_t)(w - off[s]) * 32 + lane;
-    const bool valid = o < d.dsize;
-    const uint32_t a = valid ? ldo(d.drv, o) : INF;
-    bool fail = false;
-#pragma unroll
-    for (int q = 0; q < K - 1; ++q) {
-      if (!((d.lists >> q) & 1u)) continue;
-      bool found;
-      const uint32_t* B = nbr + d.start[q];
-      const uint32_t nb = d.len[q];
-      if (A.g.ehash) {
-        // a is inside [lo, hi) already, so membership in the restricted list is edge existence
-        found = valid && edge_lookup(A.g.ehash, A.g.ehash_mask, a, d.owner[q]);
-      } else if (nb <= 32) {
-        found = warp_contains((uint32_t)lane < nb ? ldo(B, (uint32_t)lane) : INF, a);
-      } else {
-        // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then a short per-lane search
-        const uint32_t step = nb / 33u;
-        const uint32_t sp = ldo(B, (uint32_t)(lane + 1) * step);
-        int c = 0;
-#pragma unroll
-        for (int sh = 16; sh >= 1; sh >>= 1) {
-          const uint32_t t = __shfl_sync(FULL, sp, c + sh - 1);
-          if (t < a) c += sh;
-        }
-        c += __shfl_sync(FULL, sp, c) < a ? 1 : 0;  // c = #splitters < a, in [0, 32]
-        const uint32_t lo = c ? (uint32_t)c * step + 1 : 0;
-        const uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step : nb;
-        const uint32_t at = lb_thread(B, lo, hi, a);
-        found = at < nb && ldo(B, at) == a;
-      }
-      fail = fail || (found == (bool)((d.outs >> q) & 1u));
+  unsigned long long w = w0;
+  while (w < w1) {
+    // s = last sample with off[s] <= w (offsets are non-decreasing: a prefix test)
+    for (;;) {
+      const unsigned long long t = s + 1 + lane;
+      const unsigned m = __ballot_sync(FULL, t <= A.count && off[t] <= w);
+      s += __popc(m);
+      if (m != FULL) break;
     }
-    const unsigned bal = __ballot_sync(FULL, valid && fail);
-    if (lane == 0) A.bitmap[w] = bal;
+    const unsigned long long we = min(w1, off[s + 1]);
+    const IsectDesc<K>& d = desc[s];
+    for (; w < we; ++w) {
+      const uint32_t o = (uint32_t)(w - off[s]) * 32 + lane;
+      const bool valid = o < d.dsize;
+      const uint32_t a = valid ? ldo(d.drv, o) : INF;
+      bool fail = false;
+#pragma unroll
+      for (int q = 0; q < K - 1; ++q) {
+        if (!((d.lists >> q) & 1u)) continue;
+        bool found;
+        if ((d.core >> q) & 1u) {
+          // a is inside the step's [lo, hi): membership in the restricted list is edge existence
+          found = valid && core_has_edge(A.g, d.owner[q], a);
+        } else {
+          const uint32_t* B = nbr + d.start[q];
+          const uint32_t nb = d.len[q];
+          if (A.g.ehash) {
+            found = valid && edge_lookup(A.g.ehash, A.g.ehash_mask, a, d.owner[q]);
+          } else if (nb <= 32) {
+            found = warp_contains((uint32_t)lane < nb ? ldo(B, (uint32_t)lane) : INF, a);
+          } else {
+            // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then a short per-lane search
+            const uint32_t step = nb / 33u;
+            const uint32_t sp = ldo(B, (uint32_t)(lane + 1) * step);
+            int c = 0;
+#pragma unroll
+            for (int sh = 16; sh >= 1; sh >>= 1) {
+              const uint32_t t = __shfl_sync(FULL, sp, c + sh - 1);
+              if (t < a) c += sh;
+            }
+            c += __shfl_sync(FULL, sp, c) < a ? 1 : 0;  // c = #splitters < a, in [0, 32]
+            const uint32_t lo = c ? (uint32_t)c * step + 1 : 0;
+            const uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step : nb;
+            const uint32_t at = lb_thread(B, lo, hi, a);
+            found = at < nb && ldo(B, at) == a;
+          }
+        }
+        fail = fail || (found == (bool)((d.outs >> q) & 1u));
+      }
+      const unsigned bal = __ballot_sync(FULL, valid && fail);
+      if (lane == 0) A.bitmap[w] = bal;
+    }
   }
 }
 

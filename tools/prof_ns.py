@@ -7,6 +7,8 @@ import paper_2405_03488_b200 as A
 strategy = sys.argv[1] if len(sys.argv) > 1 else "frontier"
 pattern = sys.argv[2] if len(sys.argv) > 2 else "4clique"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+core = int(sys.argv[4]) if len(sys.argv) > 4 else 16384
+A.set_core_dim(core)
 g = A.rmat(20, 16, seed=1).relabel_by_degree()
 dg = A.DeviceGraph(g)
 plan = A.compile_plan(pattern)
@@ -18,4 +20,4 @@ for r in range(reps):
     torch.cuda.synchronize(); t = time.perf_counter()
     A.sample_dev(dg, plan, 1, r * B, B, vals.data_ptr(), st.cuda_stream)
     torch.cuda.synchronize(); dt = time.perf_counter() - t
-    print(f"{strategy} {pattern} rep {r}: {dt*1e3:.2f} ms  {B/dt:.3e} samples/s  hits {(vals != 0).float().mean().item():.4f}")
+    print(f"{strategy} core={core} {pattern} rep {r}: {dt*1e3:.2f} ms  {B/dt:.3e} samples/s  hits {(vals != 0).float().mean().item():.4f}")
