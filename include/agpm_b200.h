@@ -224,7 +224,7 @@ int agpm_ns_set_strategy(int strategy);
 int agpm_ns_set_frontier_reuse(int on);
 /* frontier only: dimension C of the dense-core adjacency bit matrix (top C ids,
  * C*C/8 bytes, kept in L2) that answers core-core membership tests in one
- * load; 0 disables; default 16384. Results are identical either way. */
+ * load; 0 disables; default 32768. Results are identical either way. */
 int agpm_ns_set_core_dim(uint32_t dim);
 
 /* Device-pointer building blocks (bench / multi-rank driver): enqueue only.

@@ -592,7 +592,7 @@ def set_strategy(name):
 
 
 def set_core_dim(dim):
-    """Dense-core bit-matrix dimension for the frontier sampler (0 = off, default 16384)."""
+    """Dense-core bit-matrix dimension for the frontier sampler (0 = off, default 32768)."""
     _check(lib().agpm_ns_set_core_dim(int(dim)))
 
 

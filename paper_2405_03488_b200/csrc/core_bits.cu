@@ -4,11 +4,12 @@
 // vertices, and eager-verify candidates always sit above the bound vertices'
 // ids for clique-like steps — so most membership tests "a in N(w)" of the
 // intersection phase have both a and w among the top ids. For the top C ids
-// (the "core", default C = 16384 -> a 32 MB matrix that stays in the 126 MB L2)
+// (the "core", default C = 32768 -> a 128 MB matrix; its hot rows stay in the 126 MB L2)
 // the adjacency is kept as a C x C bit matrix: a core test is ONE L2 word load
 // per lane instead of a splitter load, a shuffle search and a dependent
-// per-lane search. Measured on config 2: 92 % of the isect membership tests
-// fall inside a 16 K core (tools: profiles/r1/README.md).
+// per-lane search. On config 2, 92 % / 97.7 % of the isect membership tests
+// fall inside a 16 K / 32 K core, and one 2^24-sample 4-clique launch drops
+// from 27.2 ms to 15.9 ms (profiles/r1/README.md).
 //
 // Exact by construction (it is the adjacency restricted to [base, n)), so it
 // changes no result; it only replaces how membership is answered.
@@ -20,7 +21,7 @@
 namespace agpm_b200 {
 namespace {
 
-uint32_t g_core_dim = 16384;
+uint32_t g_core_dim = 32768;
 
 // one warp per core row: build the row in shared memory, then write it out
 __global__ void __launch_bounds__(256) core_rows_kernel(const VtxInfo* __restrict__ vtx,

@@ -57,7 +57,7 @@ struct __align__(16) IsectDesc {
   uint32_t outs;                      // bit q: ... and an out-list (difference)
   uint32_t drv_pos;                   // position owning the driver list, NO_DRV for survivors
   uint32_t drv_rs;                    // driver range start relative to that list
-  uint32_t core;                      // bit q: list q is answered by the dense-core bit matrix
+  uint32_t core;                      // bit q: list q's owner is a core vertex; bit 31: driver >= core base
 };
 
 struct FrontierArgs {
@@ -306,9 +306,11 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
     d.drv = dptr;
     d.dsize = dsize;
     d.lists = d.outs = d.core = 0;
-    // every driver element is >= lo: with lo inside the core, a list whose owner
-    // is a core vertex is answered by one bit of the core matrix
-    const bool drv_in_core = A.g.core && lo >= A.g.core_base;
+    // a list whose owner is a core vertex is answered by one bit of the core
+    // matrix for driver words inside the core; every driver element is >= lo,
+    // so lo inside the core settles that for all words (bit 31), otherwise the
+    // isect kernel checks each word's first element
+    const bool use_core = A.g.core != nullptr;
 #pragma unroll
     for (int q = 0; q < K - 1; ++q) {
       d.start[q] = 0;
@@ -320,9 +322,10 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
         d.len[q] = is_out ? S.pd[q] : re[q] - rs[q];
         d.lists |= 1u << q;
         if (is_out) d.outs |= 1u << q;
-        if (drv_in_core && S.bnd[q] >= A.g.core_base) d.core |= 1u << q;
+        if (use_core && S.bnd[q] >= A.g.core_base) d.core |= 1u << q;
       }
     }
+    if (d.core && lo >= A.g.core_base) d.core |= 1u << 31;
     d.drv_pos = reuse ? NO_DRV : (uint32_t)drv;
     d.drv_rs = drs;
     reinterpret_cast<IsectDesc<K>*>(A.desc)[i] = d;
@@ -420,12 +423,14 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
       const uint32_t o = (uint32_t)(w - off[s]) * 32 + lane;
       const bool valid = o < d.dsize;
       const uint32_t a = valid ? ldo(d.drv, o) : INF;
+      uint32_t core = d.core;
+      if (core && !(core >> 31) && __shfl_sync(FULL, a, 0) < A.g.core_base) core = 0;  // word leaves the core
       bool fail = false;
 #pragma unroll
       for (int q = 0; q < K - 1; ++q) {
         if (!((d.lists >> q) & 1u)) continue;
         bool found;
-        if ((d.core >> q) & 1u) {
+        if ((core >> q) & 1u) {
           // a is inside the step's [lo, hi): membership in the restricted list is edge existence
           found = valid && core_has_edge(A.g, d.owner[q], a);
         } else {

@@ -42,11 +42,11 @@ def strategy(agpm, request):
     agpm.set_frontier_reuse(request.param == "frontier_reuse")
     # frontier: the dense-core bit matrix covers every vertex of the small test
     # graphs by default; "nocore" runs the splitter-search path instead
-    agpm.set_core_dim(0 if request.param == "frontier_nocore" else 16384)
+    agpm.set_core_dim(0 if request.param == "frontier_nocore" else 32768)
     yield request.param
     agpm.set_strategy("auto")
     agpm.set_frontier_reuse(False)
-    agpm.set_core_dim(16384)
+    agpm.set_core_dim(32768)
 
 
 @pytest.mark.parametrize("name", ["er200", "er200_rel", "er60_dense", "rmat12_rel", "rmat12"])
