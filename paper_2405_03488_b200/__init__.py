@@ -583,11 +583,11 @@ def window_moments_dev(d_values_ptr, count, window, d_out_ptr, stream=None):
                                          None if stream is None else C.c_void_p(stream)))
 
 
-STRATEGIES = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3}
+STRATEGIES = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3, "fused": 4}
 
 
 def set_strategy(name):
-    """Sampler kernel choice (all draw identical samples): auto | warp | lane | frontier."""
+    """Sampler kernel choice (all draw identical samples): auto | warp | lane | frontier | fused."""
     _check(lib().agpm_ns_set_strategy(STRATEGIES[name]))
 
 

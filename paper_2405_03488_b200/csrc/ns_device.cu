@@ -187,7 +187,7 @@ GraphArgs graph_args(const agpm_graph* g) {
 // Strategy: one warp per sample (coalesced chunk intersections, k-ary
 // searches) unless adjacency lists are tiny, where one lane per sample keeps
 // 32 samples in flight per warp. Override with agpm_ns_set_strategy().
-constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3;
+constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3, kStrategyFused = 4;
 int g_strategy = kStrategyAuto;
 
 int choose_strategy(const agpm_graph* g, uint64_t count) {
@@ -211,7 +211,7 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
     return;
   }
   const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, count);  // B_min replay: warp kernel
-  if (strat == kStrategyFrontier) ensure_core_bits(const_cast<agpm_graph*>(g), s);
+  if (strat == kStrategyFrontier || strat == kStrategyFused) ensure_core_bits(const_cast<agpm_graph*>(g), s);
   // (the edge-hash membership path is available but off: on RMAT-20 it turned
   // L2-local list searches into random HBM sectors and ran 2.6x slower)
   SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};
@@ -219,6 +219,8 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
     launch_ns_lane(L, s);
   else if (strat == kStrategyFrontier)
     launch_ns_frontier(L, s);
+  else if (strat == kStrategyFused)
+    launch_ns_fused(L, s);
   else
     launch_ns_warp(L, s);
 }
@@ -246,8 +248,8 @@ extern "C" {
 
 int agpm_ns_set_strategy(int strategy) {
   return guarded([&] {
-    if (strategy < 0 || strategy > 3)
-      throw std::invalid_argument("strategy must be 0 (auto), 1 (warp), 2 (lane) or 3 (frontier)");
+    if (strategy < 0 || strategy > 4)
+      throw std::invalid_argument("strategy must be 0 (auto), 1 (warp), 2 (lane), 3 (frontier) or 4 (fused)");
     g_strategy = strategy;
   });
 }

@@ -189,7 +189,7 @@ __device__ void load_state(const FrontierArgs& A, unsigned long long i, Sample<K
 template <int K>
 __device__ void finish(const FrontierArgs& A, unsigned long long i, const Sample<K>& S, int nb, bool hit) {
   A.values[i] = hit ? S.alpha : 0.0;
-  A.work[i] = 0;
+  if (A.work) A.work[i] = 0;
   if (A.bindings) {
 #pragma unroll
     for (int q = 0; q < K; ++q) A.bindings[i * K + q] = q < nb ? S.bnd[q] : INF;
@@ -212,9 +212,12 @@ __device__ __forceinline__ void step_bounds(const DevPlan& p, int s, const Sampl
 // multi-list step after writing its descriptor, or finish the sample. With
 // `surv` set, step s0 uses those survivors of step s0-1 as its driver and only
 // the lists step s0-1 did not have.
+// Returns the step whose descriptor was written (pending intersection), or -1
+// once the sample is finished. With `local` set (fused kernel) the descriptor
+// goes there and nothing is written to the SoA state.
 template <int K>
-__device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& S, int s0, const uint32_t* surv,
-                        uint32_t surv_len) {
+__device__ int advance(const FrontierArgs& A, unsigned long long i, Sample<K>& S, int s0, const uint32_t* surv,
+                       uint32_t surv_len, IsectDesc<K>* local = nullptr) {
   const uint32_t* __restrict__ nbr = A.g.nbr;
   const DevPlan& p = A.p;
 #pragma unroll
@@ -259,7 +262,7 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
     }
     if (dsize == 0) {
       finish(A, i, S, j, false);
-      return;
+      return -1;
     }
     if (!A.step_multi[s]) {
       // single list: |S| = |range| - bound vertices inside it, pick by index
@@ -279,7 +282,7 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
       const uint32_t cnt = dsize - nex;
       if (cnt == 0) {
         finish(A, i, S, j, false);
-        return;
+        return -1;
       }
       const uint32_t r = (uint32_t)S.rng.next_below(cnt);
       uint32_t o = r;
@@ -328,12 +331,17 @@ __device__ void advance(const FrontierArgs& A, unsigned long long i, Sample<K>& 
     if (d.core && lo >= A.g.core_base) d.core |= 1u << 31;
     d.drv_pos = reuse ? NO_DRV : (uint32_t)drv;
     d.drv_rs = drs;
+    if (local) {
+      *local = d;
+      return s;
+    }
     reinterpret_cast<IsectDesc<K>*>(A.desc)[i] = d;
     A.work[i] = (dsize + 31) >> 5;
     store_state(A, i, S, j);
-    return;
+    return s;
   }
   finish(A, i, S, K, true);
+  return -1;
 }
 
 template <int K>
@@ -591,6 +599,175 @@ __global__ void __launch_bounds__(256) fr_pick_kernel(const FrontierArgs A, int 
   }
 }
 
+// Fused sampler: one warp owns 32 samples (lane l <-> sample base + l).
+// Scalar work (seed, bounds, ranges, driver choice, single-list steps) runs
+// lane-parallel exactly as in fr_seed/fr_pick; each lane leaves its step
+// descriptor in shared memory, and the warp then intersects the pending
+// samples one after another, all 32 lanes on one sample's driver words (core
+// bit tests or splitter searches, as in fr_isect), counts |S_j| from the live
+// ballots, draws r with that sample's own CounterRng (broadcast, evaluated
+// uniformly) and selects the r-th live element from the per-lane ballot words.
+// No per-sample state leaves the SM between steps: no SoA state, scans,
+// bitmaps or host round trips.
+template <int K>
+__device__ __forceinline__ unsigned live_word(const FrontierArgs& A, const IsectDesc<K>& d, uint32_t core, uint32_t w,
+                                              int lane, int j) {
+  const uint32_t* __restrict__ nbr = A.g.nbr;
+  const uint32_t o = w * 32 + lane;
+  const bool valid = o < d.dsize;
+  const uint32_t a = valid ? ldo(d.drv, o) : INF;
+  if (core && !(core >> 31) && __shfl_sync(FULL, a, 0) < A.g.core_base) core = 0;
+  bool fail = !valid;
+#pragma unroll
+  for (int q = 0; q < K - 1; ++q) {
+    if (q < j && a == d.owner[q]) fail = true;  // bound vertices are not candidates (walker.hpp:70-82)
+    if (!((d.lists >> q) & 1u)) continue;
+    bool found;
+    if ((core >> q) & 1u) {
+      found = valid && core_has_edge(A.g, d.owner[q], a);
+    } else {
+      const uint32_t* B = nbr + d.start[q];
+      const uint32_t nb = d.len[q];
+      if (nb <= 32) {
+        found = warp_contains((uint32_t)lane < nb ? ldo(B, (uint32_t)lane) : INF, a);
+      } else {
+        const uint32_t step = nb / 33u;
+        const uint32_t sp = ldo(B, (uint32_t)(lane + 1) * step);
+        int c = 0;
+#pragma unroll
+        for (int sh = 16; sh >= 1; sh >>= 1) {
+          const uint32_t t = __shfl_sync(FULL, sp, c + sh - 1);
+          if (t < a) c += sh;
+        }
+        c += __shfl_sync(FULL, sp, c) < a ? 1 : 0;
+        const uint32_t lo = c ? (uint32_t)c * step + 1 : 0;
+        const uint32_t hi = c < 32 ? (uint32_t)(c + 1) * step : nb;
+        const uint32_t at = lb_thread(B, lo, hi, a);
+        found = at < nb && ldo(B, at) == a;
+      }
+    }
+    fail = fail || (found == (bool)((d.outs >> q) & 1u));
+  }
+  return __ballot_sync(FULL, !fail);
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) fr_fused_kernel(const FrontierArgs A) {
+  __shared__ IsectDesc<K> sdesc[256];
+  const int lane = threadIdx.x & 31;
+  IsectDesc<K>* wdesc = sdesc + (threadIdx.x & ~31u);
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long base = (blockIdx.x * (unsigned long long)blockDim.x) + (threadIdx.x & ~31u);
+       base < A.count; base += stride) {
+    const unsigned long long i = base + lane;
+    const bool act = i < A.count;
+    Sample<K> S(A.seed, A.first_id + (act ? i : 0));
+    int pend = -1;
+    if (act) {
+      S.alpha = A.p.alpha0;
+      const unsigned long long r0 = S.rng.next_below(A.g.arcs);  // ns_engine.cpp:29-33
+      const unsigned long long arc = __ldg(A.g.seed_arcs + r0);
+      uint32_t u = (uint32_t)(arc >> 32), v = (uint32_t)arc;
+      const bool swapped = A.p.seed_ordered && u > v;
+      if (swapped) {
+        const uint32_t t = u;
+        u = v;
+        v = t;
+      }
+      bind(S, 0, u);
+      bind(S, 1, v);
+      ensure_vtx(A.g, S, 0);
+      ensure_vtx(A.g, S, 1);
+      if (A.g.plain) {
+        if (!swapped) {
+          S.hbo[0] = (uint32_t)(r0 - S.pb[0]) + 1;
+          S.hbl[0] = v + 1;
+        } else {
+          S.hbo[1] = (uint32_t)(r0 - S.pb[1]) + 1;
+          S.hbl[1] = u + 1;
+        }
+      }
+      pend = advance<K>(A, i, S, 0, nullptr, 0, wdesc + lane);
+    }
+    for (;;) {
+      unsigned pending = __ballot_sync(FULL, pend >= 0);
+      if (!pending) break;
+      __syncwarp();
+      bool picked = false;
+      while (pending) {
+        const int src = __ffs(pending) - 1;
+        pending &= pending - 1;
+        const int step = __shfl_sync(FULL, pend, src);
+        const int j = step + 2;
+        const IsectDesc<K>& d = wdesc[src];
+        const uint32_t core = d.core;
+        const uint32_t nw = (d.dsize + 31) >> 5;
+        unsigned myword = 0;
+        unsigned long long cnt = 0;
+        for (uint32_t w = 0; w < nw; ++w) {
+          const unsigned live = live_word<K>(A, d, core, w, lane, j);
+          if ((uint32_t)lane == w) myword = live;
+          cnt += __popc(live);
+        }
+        if (cnt == 0) {
+          if (lane == src) {
+            finish(A, i, S, j, false);
+            pend = -1;
+          }
+          continue;
+        }
+        CounterRng rr(0);
+        rr.key = __shfl_sync(FULL, S.rng.key, src);
+        rr.ctr = __shfl_sync(FULL, S.rng.ctr, src);
+        unsigned long long r = rr.next_below(cnt);  // uniform: every lane runs src's stream
+        uint32_t o_pick = 0;
+        if (nw <= 32) {
+          const unsigned pc = __popc(myword);
+          unsigned incl = pc;
+#pragma unroll
+          for (int dd = 1; dd < 32; dd <<= 1) {
+            const unsigned t = __shfl_up_sync(FULL, incl, dd);
+            if (lane >= dd) incl += t;
+          }
+          const unsigned excl = incl - pc;
+          const unsigned who = __ballot_sync(FULL, excl <= r && r < incl);
+          const int wl = __ffs(who) - 1;
+          uint32_t ob = 0;
+          if (lane == wl) ob = (uint32_t)wl * 32 + __fns(myword, 0, (int)(r - excl) + 1);
+          o_pick = __shfl_sync(FULL, ob, wl);
+        } else {  // long driver: replay the words up to the r-th live element
+          for (uint32_t w = 0; w < nw; ++w) {
+            const unsigned live = live_word<K>(A, d, core, w, lane, j);
+            const unsigned pc = __popc(live);
+            if (r < pc) {
+              o_pick = w * 32 + __fns(live, 0, (int)r + 1);
+              break;
+            }
+            r -= pc;
+          }
+        }
+        const uint32_t pick = ldo(d.drv, o_pick);
+        if (lane == src) {
+          S.rng.ctr = rr.ctr;
+          S.alpha = __dmul_rn(S.alpha, (double)cnt);  // alpha *= |S_j| (ns_engine.cpp:39)
+          if (d.drv_pos != NO_DRV) {
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+              if ((uint32_t)q == d.drv_pos) {  // lower_bound(pick + 1) = drv_rs + o + 1
+                S.hbo[q] = d.drv_rs + o_pick + 1;
+                S.hbl[q] = pick + 1;
+              }
+          }
+          bind(S, j, pick);
+          picked = true;
+        }
+      }
+      __syncwarp();
+      if (picked) pend = advance<K>(A, i, S, pend + 1, nullptr, 0, wdesc + lane);
+    }
+  }
+}
+
 // Nested survivor reuse is exact but, at word granularity, rarely cheaper than
 // re-intersecting (a sample's step-j driver is ~1 bitmap word either way) while
 // compaction makes the pick phase divergent; off unless enabled.
@@ -691,9 +868,53 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
   }
 }
 
+template <int K>
+void run_fused_k(const SampleLaunch& L, cudaStream_t s) {
+  DeviceCtx& ctx = ctx_for_current_device();
+  FrontierArgs A{};
+  A.g = L.g;
+  A.p = L.p;
+  A.seed = L.seed;
+  A.first_id = L.first_id;
+  A.count = L.count;
+  A.values = L.values;
+  A.bindings = L.bindings;
+  for (int st = 0; st < K - 2; ++st) {
+    const unsigned in_m = L.p.in_mask[st], out_m = L.p.out_mask[st];
+    A.step_multi[st] = !(__builtin_popcount(in_m) == 1 && out_m == 0);
+    A.step_reuse[st] = 0;
+  }
+  static int occ = -1;
+  if (occ < 0) {
+    int o = 0;
+    AGPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fr_fused_kernel<K>, 256, 0));
+    occ = o > 0 ? o : 1;
+  }
+  const unsigned blocks =
+      (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>((L.count + 255) / 256,
+                                                                             (unsigned long long)ctx.sm_count * occ));
+  fr_fused_kernel<K><<<blocks, 256, 0, s>>>(A);
+  count_launch();
+  AGPM_CUDA(cudaGetLastError());
+}
+
 }  // namespace
 
 void set_frontier_reuse(bool on) { g_frontier_reuse = on; }
+
+void launch_ns_fused(const SampleLaunch& L, cudaStream_t s) {
+  if (L.bytes_out) throw std::invalid_argument("B_min accounting runs on the warp sampler");
+  switch (L.p.k) {
+    case 3: run_fused_k<3>(L, s); break;
+    case 4: run_fused_k<4>(L, s); break;
+    case 5: run_fused_k<5>(L, s); break;
+    case 6: run_fused_k<6>(L, s); break;
+    case 7: run_fused_k<7>(L, s); break;
+    case 8: run_fused_k<8>(L, s); break;
+    case 9: run_fused_k<9>(L, s); break;
+    default: throw std::invalid_argument("device sampler needs 3 <= k <= 9");
+  }
+}
 
 void launch_ns_frontier(const SampleLaunch& L, cudaStream_t s) {
   if (L.bytes_out) throw std::invalid_argument("B_min accounting runs on the warp sampler");

@@ -36,13 +36,13 @@ def graphs(agpm):
     return _graphs(agpm)
 
 
-@pytest.fixture(params=["warp", "lane", "frontier", "frontier_reuse", "frontier_nocore"])
+@pytest.fixture(params=["warp", "lane", "frontier", "frontier_reuse", "frontier_nocore", "fused", "fused_nocore"])
 def strategy(agpm, request):
     agpm.set_strategy(request.param.split("_")[0])
     agpm.set_frontier_reuse(request.param == "frontier_reuse")
     # frontier: the dense-core bit matrix covers every vertex of the small test
     # graphs by default; "nocore" runs the splitter-search path instead
-    agpm.set_core_dim(0 if request.param == "frontier_nocore" else 32768)
+    agpm.set_core_dim(0 if request.param.endswith("nocore") else 32768)
     yield request.param
     agpm.set_strategy("auto")
     agpm.set_frontier_reuse(False)
