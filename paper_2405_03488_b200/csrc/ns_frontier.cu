@@ -230,22 +230,69 @@ __device__ int advance(const FrontierArgs& A, unsigned long long i, Sample<K>& S
     const unsigned in_m = p.in_mask[s] & ~prev_in, out_m = p.out_mask[s] & ~prev_out;
     uint32_t lo, hi;
     step_bounds(p, s, S, lo, hi);
+    // Ranges [rs, re) of the in-lists inside [lo, hi). First a SUPERSET range
+    // from the hints alone (no memory traffic): up = lower_bound(bnd + 1) and
+    // hbo = lower_bound(hbl) bracket lower_bound(lo) / lower_bound(hi). Only the
+    // driver needs its exact range (it is enumerated); other lists are probed
+    // for membership of elements already inside [lo, hi), for which a superset
+    // range answers the same. Exact ranges are computed smallest-superset first
+    // until the smallest candidate is exact, so the driver is still the
+    // smallest exact range.
     uint32_t rs[K], re[K];
+    bool exact[K];
     int drv = -1, t_in = 0;
     uint32_t dsize = INF;
 #pragma unroll
     for (int q = 0; q < K; ++q) {
       rs[q] = re[q] = 0;
+      exact[q] = false;
       if (q < j && (((in_m | out_m) >> q) & 1u)) ensure_vtx(A.g, S, q);
       if (q < j && ((in_m >> q) & 1u)) {
         ++t_in;
-        rs[q] = lo ? lbq(nbr, S, q, lo, true) : 0;
-        re[q] = hi == INF ? S.pd[q] : lbq(nbr, S, q, hi, false);
-        if (re[q] < rs[q]) re[q] = rs[q];
-        if (!reuse && re[q] - rs[q] < dsize) {
-          dsize = re[q] - rs[q];
-          drv = q;
+        uint32_t L = 0, U = S.pd[q];
+        bool ex_lo = lo == 0, ex_hi = hi == INF;
+        if (lo) {
+          if (lo >= S.bnd[q] + 1) L = max(L, S.up[q]);
+          if (lo >= S.hbl[q]) L = max(L, S.hbo[q]);
+          ex_lo = lo == S.bnd[q] + 1 || lo == S.hbl[q];
         }
+        if (hi != INF) {
+          if (hi <= S.bnd[q] + 1) U = min(U, S.up[q]);
+          if (hi <= S.hbl[q]) U = min(U, S.hbo[q]);
+          ex_hi = hi == S.bnd[q] + 1 || hi == S.hbl[q];
+        }
+        rs[q] = L;
+        re[q] = max(U, L);
+        exact[q] = ex_lo && ex_hi;
+      }
+    }
+    if (!reuse) {
+#pragma unroll
+      for (int it = 0; it < K; ++it) {
+        int b = -1;
+        uint32_t bs = INF;
+        bool bex = false;
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+          if (q < j && ((in_m >> q) & 1u) && re[q] - rs[q] < bs) {
+            bs = re[q] - rs[q];
+            b = q;
+            bex = exact[q];
+          }
+        if (b < 0) break;
+        if (bex) {
+          drv = b;
+          dsize = bs;
+          break;
+        }
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+          if (q == b) {
+            rs[q] = lo ? lbq(nbr, S, q, lo, true) : 0;
+            re[q] = hi == INF ? S.pd[q] : lbq(nbr, S, q, hi, false);
+            if (re[q] < rs[q]) re[q] = rs[q];
+            exact[q] = true;
+          }
       }
     }
     const uint32_t* dptr = surv;
