@@ -138,3 +138,15 @@ def test_errors_are_loud(agpm):
     oriented = agpm.DeviceGraph(tri.orient_by_degree())
     with pytest.raises(ValueError):
         agpm.draw_samples(oriented, agpm.compile_plan("triangle"), 1, 0, 10)
+
+
+@pytest.mark.parametrize("pattern", ["triangle", "4clique", "5clique", "4cycle", "house", "4motif-diamond", "dumbbell"])
+def test_values_without_bindings(agpm, oracle, graphs, pattern, strategy):
+    """Without bindings the frontier sampler only counts the last step's
+    candidates (no pick): values must still equal the oracle's bit for bit."""
+    g = graphs["rmat12_rel"]
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan(pattern)
+    v, h, _ = agpm.draw_samples(agpm.DeviceGraph(g), plan, 4, 999, 5000, with_bindings=False)
+    ov, oh, _ = oracle.draw_records(off, nbr, g.edge_count, plan, 4, 999, 5000)
+    np.testing.assert_array_equal(v, ov)
