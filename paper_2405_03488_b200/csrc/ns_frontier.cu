@@ -440,7 +440,7 @@ __device__ __forceinline__ bool warp_contains(uint32_t b, uint32_t a) {
 // into registers, and its words follow. Core lists cost one L2 word per lane;
 // the rest load 32 splitters and finish with a short per-lane search.
 template <int K>
-__global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, unsigned long long words) {
+__global__ void __launch_bounds__(256, 8) fr_isect_kernel(const FrontierArgs A, unsigned long long words) {
   const int lane = threadIdx.x & 31;
   const unsigned long long* __restrict__ off = A.offsets;
   const IsectDesc<K>* __restrict__ desc = reinterpret_cast<const IsectDesc<K>*>(A.desc);
@@ -474,16 +474,43 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
     }
     const unsigned long long we = min(w1, off[s + 1]);
     const IsectDesc<K>& d = desc[s];
+    // loop-invariant scalars of the descriptor in registers; per-list fields stay in L1
+    const uint32_t* __restrict__ drv = d.drv;
+    const uint32_t dsize = d.dsize, lists = d.lists, outs = d.outs, core0 = d.core;
+    const unsigned long long wbase = off[s];
+    if (core0 == (lists | (1u << 31)) && outs == 0 && __popc(lists) <= 2) {
+      // fast path (the common case on a relabelled graph): every other list is
+      // a core row and the whole driver lies inside the core -> per word one
+      // coalesced driver load and one bit probe per list
+      const int q0 = __ffs(lists) - 1;
+      const int q1 = __popc(lists) == 2 ? 31 - __clz(lists) : -1;
+      const uint32_t cb = A.g.core_base;
+      const uint32_t* r0 = A.g.core + (unsigned long long)(d.owner[q0] - cb) * A.g.core_wpr;
+      const uint32_t* r1 = q1 >= 0 ? A.g.core + (unsigned long long)(d.owner[q1] - cb) * A.g.core_wpr : r0;
+      for (; w < we; ++w) {
+        const uint32_t o = (uint32_t)(w - wbase) * 32 + lane;
+        bool fail = false;
+        if (o < dsize) {
+          const uint32_t c = ldo(drv, o) - cb;
+          const uint32_t b0 = __ldg(r0 + (c >> 5));
+          const uint32_t b1 = __ldg(r1 + (c >> 5));
+          fail = !((b0 & b1) >> (c & 31) & 1u);
+        }
+        const unsigned bal = __ballot_sync(FULL, fail);
+        if (lane == 0) A.bitmap[w] = bal;
+      }
+      continue;
+    }
     for (; w < we; ++w) {
-      const uint32_t o = (uint32_t)(w - off[s]) * 32 + lane;
-      const bool valid = o < d.dsize;
-      const uint32_t a = valid ? ldo(d.drv, o) : INF;
-      uint32_t core = d.core;
+      const uint32_t o = (uint32_t)(w - wbase) * 32 + lane;
+      const bool valid = o < dsize;
+      const uint32_t a = valid ? ldo(drv, o) : INF;
+      uint32_t core = core0;
       if (core && !(core >> 31) && __shfl_sync(FULL, a, 0) < A.g.core_base) core = 0;  // word leaves the core
       bool fail = false;
 #pragma unroll
       for (int q = 0; q < K - 1; ++q) {
-        if (!((d.lists >> q) & 1u)) continue;
+        if (!((lists >> q) & 1u)) continue;
         bool found;
         if ((core >> q) & 1u) {
           // a is inside the step's [lo, hi): membership in the restricted list is edge existence
@@ -512,7 +539,7 @@ __global__ void __launch_bounds__(256) fr_isect_kernel(const FrontierArgs A, uns
             found = at < nb && ldo(B, at) == a;
           }
         }
-        fail = fail || (found == (bool)((d.outs >> q) & 1u));
+        fail = fail || (found == (bool)((outs >> q) & 1u));
       }
       const unsigned bal = __ballot_sync(FULL, valid && fail);
       if (lane == 0) A.bitmap[w] = bal;
