@@ -42,7 +42,7 @@ namespace agpm_b200 {
 namespace {
 
 constexpr uint32_t INF = 0xffffffffu;
-constexpr unsigned long long kFrontierCap = 1ull << 22;  // samples per pass
+constexpr unsigned long long kFrontierCap = 1ull << 24;  // samples per pass
 constexpr uint32_t NO_DRV = 0xffffffffu;
 
 // Per-sample intersection job; other-list slots are indexed by matching position.
