@@ -218,8 +218,10 @@ int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delt
  * (k-ary searches + coalesced chunk intersections), 2 = one lane per sample
  * (tiny adjacency lists), 3 = frontier phases (element-parallel
  * intersections over a whole batch), 4 = fused (a warp owns 32 samples: scalar
- * work lane-parallel, intersections warp-cooperative, state kept on chip).
- * All strategies draw identical samples. */
+ * work lane-parallel, intersections warp-cooperative, state kept on chip),
+ * 5 = flat (a warp owns 32 samples, state on chip; each multi-list step
+ * intersects the concatenation of the pending samples' drivers element-parallel,
+ * picks lane-parallel). All strategies draw identical samples. */
 int agpm_ns_set_strategy(int strategy);
 /* frontier only: let a step whose lists nest the previous step's (cliques)
  * intersect that step's survivors instead of recomputing (same samples). */

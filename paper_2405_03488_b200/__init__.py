@@ -583,7 +583,7 @@ def window_moments_dev(d_values_ptr, count, window, d_out_ptr, stream=None):
                                          None if stream is None else C.c_void_p(stream)))
 
 
-STRATEGIES = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3, "fused": 4}
+STRATEGIES = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3, "fused": 4, "flat": 5}
 
 
 def set_strategy(name):

@@ -187,11 +187,23 @@ GraphArgs graph_args(const agpm_graph* g) {
 // Strategy: one warp per sample (coalesced chunk intersections, k-ary
 // searches) unless adjacency lists are tiny, where one lane per sample keeps
 // 32 samples in flight per warp. Override with agpm_ns_set_strategy().
-constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3, kStrategyFused = 4;
+constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3, kStrategyFused = 4, kStrategyFlat = 5;
 int g_strategy = kStrategyAuto;
 
-int choose_strategy(const agpm_graph* g, uint64_t count) {
+// clique plans (every step intersects all bound vertices' lists, no out-lists):
+// their drivers are short suffixes answered by the dense core, where the flat
+// sampler wins (config 2, per 2^24 samples: triangle 6.2 vs 7.8 ms, 4-clique
+// 9.3 vs 12.8, 5-clique 14.7 vs 18.3); elsewhere (4-cycle 10.9 vs 9.9, house
+// 170 vs 82) long non-core drivers favour the frontier phases
+bool clique_plan(const DevPlan& p) {
+  for (int s = 0; s < p.k - 2; ++s)
+    if (p.in_mask[s] != (1u << (s + 2)) - 1u || p.out_mask[s] != 0) return false;
+  return true;
+}
+
+int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count) {
   if (g_strategy != kStrategyAuto) return g_strategy;
+  if (count >= (1ull << 18) && clique_plan(p)) return kStrategyFlat;
   const double avg_deg = g->n ? static_cast<double>(g->arcs) / g->n : 0.0;
   if (avg_deg <= 24.0 && g->max_degree <= 256) return kStrategyLane;
   return count >= (1ull << 18) ? kStrategyFrontier : kStrategyWarp;
@@ -210,8 +222,8 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
     launch_ns_lazy(L, s);
     return;
   }
-  const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, count);  // B_min replay: warp kernel
-  if (strat == kStrategyFrontier || strat == kStrategyFused) ensure_core_bits(const_cast<agpm_graph*>(g), s);
+  const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, dp, count);  // B_min replay: warp kernel
+  if (strat == kStrategyFrontier || strat == kStrategyFused || strat == kStrategyFlat) ensure_core_bits(const_cast<agpm_graph*>(g), s);
   // (the edge-hash membership path is available but off: on RMAT-20 it turned
   // L2-local list searches into random HBM sectors and ran 2.6x slower)
   SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};
@@ -221,6 +233,8 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
     launch_ns_frontier(L, s);
   else if (strat == kStrategyFused)
     launch_ns_fused(L, s);
+  else if (strat == kStrategyFlat)
+    launch_ns_flat(L, s);
   else
     launch_ns_warp(L, s);
 }
@@ -248,8 +262,8 @@ extern "C" {
 
 int agpm_ns_set_strategy(int strategy) {
   return guarded([&] {
-    if (strategy < 0 || strategy > 4)
-      throw std::invalid_argument("strategy must be 0 (auto), 1 (warp), 2 (lane), 3 (frontier) or 4 (fused)");
+    if (strategy < 0 || strategy > 5)
+      throw std::invalid_argument("strategy must be 0 (auto), 1 (warp), 2 (lane), 3 (frontier), 4 (fused) or 5 (flat)");
     g_strategy = strategy;
   });
 }

@@ -36,7 +36,7 @@ def graphs(agpm):
     return _graphs(agpm)
 
 
-@pytest.fixture(params=["warp", "lane", "frontier", "frontier_reuse", "frontier_nocore", "fused", "fused_nocore"])
+@pytest.fixture(params=["warp", "lane", "frontier", "frontier_reuse", "frontier_nocore", "fused", "fused_nocore", "flat", "flat_nocore"])
 def strategy(agpm, request):
     agpm.set_strategy(request.param.split("_")[0])
     agpm.set_frontier_reuse(request.param == "frontier_reuse")
@@ -63,6 +63,32 @@ def test_draw_bit_exact(agpm, oracle, graphs, name, pattern, strategy):
     ov, oh, ob = oracle.draw_records(off, nbr, m, plan, 9, first, count)
     np.testing.assert_array_equal(h, oh)
     np.testing.assert_array_equal(v, ov)  # bit-exact doubles
+    np.testing.assert_array_equal(b, ob)
+
+
+@pytest.mark.parametrize("relabel", [False, True])
+@pytest.mark.parametrize("pattern", ["triangle", "4clique", "4cycle", "house", "4motif-diamond"])
+@pytest.mark.parametrize("strat", ["flat", "flat_nocore", "frontier"])
+def test_long_drivers_bit_exact(agpm, oracle, pattern, relabel, strat):
+    """RMAT-16 hubs (degree > 2048): drivers longer than the flat sampler's
+    round capacity take its warp-per-sample path; values and bindings still
+    match the oracle record for record."""
+    g = agpm.rmat(16, 16, seed=5)
+    if relabel:
+        g = g.relabel_by_degree()
+    assert g.max_degree() > 4096
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan(pattern)
+    dg = agpm.DeviceGraph(g)
+    agpm.set_strategy(strat.split("_")[0])
+    agpm.set_core_dim(0 if strat.endswith("nocore") else 32768)
+    try:
+        v, h, b = agpm.draw_samples(dg, plan, 4, 777, 20000)
+    finally:
+        agpm.set_strategy("auto")
+        agpm.set_core_dim(32768)
+    ov, oh, ob = oracle.draw_records(off, nbr, g.edge_count, plan, 4, 777, 20000)
+    np.testing.assert_array_equal(v, ov)
     np.testing.assert_array_equal(b, ob)
 
 

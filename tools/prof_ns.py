@@ -9,7 +9,11 @@ pattern = sys.argv[2] if len(sys.argv) > 2 else "4clique"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 core = int(sys.argv[4]) if len(sys.argv) > 4 else 16384
 A.set_core_dim(core)
-g = A.rmat(20, 16, seed=1).relabel_by_degree()
+graph = sys.argv[5] if len(sys.argv) > 5 else "rmat20"
+if graph == "er10k":  # config 1
+    g = A.er_graph(10000, 20 / 9999, 1).relabel_by_degree()
+else:
+    g = A.rmat(int(graph[4:]), 16, seed=1).relabel_by_degree()
 dg = A.DeviceGraph(g)
 plan = A.compile_plan(pattern)
 A.set_strategy(strategy)
@@ -20,4 +24,4 @@ for r in range(reps):
     torch.cuda.synchronize(); t = time.perf_counter()
     A.sample_dev(dg, plan, 1, r * B, B, vals.data_ptr(), st.cuda_stream)
     torch.cuda.synchronize(); dt = time.perf_counter() - t
-    print(f"{strategy} core={core} {pattern} rep {r}: {dt*1e3:.2f} ms  {B/dt:.3e} samples/s  hits {(vals != 0).float().mean().item():.4f}")
+    print(f"{strategy} core={core} {graph} {pattern} rep {r}: {dt*1e3:.2f} ms  {B/dt:.3e} samples/s  hits {(vals != 0).float().mean().item():.4f}")
