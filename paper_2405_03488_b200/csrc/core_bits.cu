@@ -58,7 +58,7 @@ void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
   if (g->core && g->core_dim == want) return;
   if (g->core) {
     AGPM_CUDA(cudaStreamSynchronize(s));
-    AGPM_CUDA(cudaFree(g->core));
+    AGPM_CUDA(dev_free(g->core));
     g->bytes -= 4ull * g->core_wpr * g->core_dim;
     g->core = nullptr;
     g->core_dim = g->core_wpr = g->core_base = 0;
@@ -68,7 +68,7 @@ void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
   const uint32_t base = g->n - want;
   const uint32_t wpr = (want + 31) / 32;
   uint32_t* bits = nullptr;
-  AGPM_CUDA(cudaMalloc(&bits, 4ull * wpr * want));
+  AGPM_CUDA(dev_malloc(&bits, 4ull * wpr * want));
   const size_t shmem = 8ull * 4 * wpr;
   if (shmem > 48 * 1024)
     AGPM_CUDA(cudaFuncSetAttribute(core_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));

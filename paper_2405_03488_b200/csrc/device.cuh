@@ -48,6 +48,18 @@ struct DeviceCtx {
 };
 
 DeviceCtx& ctx_for_current_device();
+
+// Device memory comes from the device's stream-ordered pool (release threshold
+// unbounded): creating and dropping graph views, sparsified copies and
+// scratch reuses cached memory instead of paying cudaMalloc/cudaFree each time.
+// dev_malloc returns memory usable on any stream; dev_free keeps cudaFree's
+// device-wide synchronisation.
+cudaError_t dev_malloc_bytes(void** p, size_t bytes);
+cudaError_t dev_free(void* p);
+template <class T>
+cudaError_t dev_malloc(T** p, size_t bytes) {
+  return dev_malloc_bytes(reinterpret_cast<void**>(p), bytes);
+}
 cudaStream_t pick_stream(void* stream);
 void count_launch(uint64_t n = 1);
 

@@ -18,6 +18,20 @@ DeviceCtx* g_ctx[64] = {nullptr};
 }  // namespace
 
 void set_last_error(const std::string& msg) { t_err = msg; }
+
+cudaError_t dev_malloc_bytes(void** p, size_t bytes) {
+  cudaStream_t s = ctx_for_current_device().stream;
+  cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
+cudaError_t dev_free(void* p) {
+  if (!p) return cudaSuccess;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return e;
+  return cudaFreeAsync(p, ctx_for_current_device().stream);
+}
 void count_launch(uint64_t n) { g_launches += n; }
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -31,9 +45,9 @@ void cuda_check(cudaError_t e, const char* what) {
 
 void* DeviceCtx::get(int slot, size_t bytes) {
   if (scratch_bytes[slot] < bytes) {
-    if (scratch[slot]) AGPM_CUDA(cudaFree(scratch[slot]));
+    if (scratch[slot]) AGPM_CUDA(dev_free(scratch[slot]));
     size_t grow = bytes + bytes / 4;
-    AGPM_CUDA(cudaMalloc(&scratch[slot], grow));
+    AGPM_CUDA(dev_malloc(&scratch[slot], grow));
     scratch_bytes[slot] = grow;
   }
   return scratch[slot];
@@ -41,7 +55,7 @@ void* DeviceCtx::get(int slot, size_t bytes) {
 
 uint32_t* alloc_nbr(uint64_t len, cudaStream_t s) {
   uint32_t* p = nullptr;
-  AGPM_CUDA(cudaMalloc(&p, 4ull * (len + kNbrPad)));
+  AGPM_CUDA(dev_malloc(&p, 4ull * (len + kNbrPad)));
   AGPM_CUDA(cudaMemsetAsync(p + len, 0, 4ull * kNbrPad, s));
   return p;
 }
@@ -68,6 +82,10 @@ DeviceCtx& ctx_for_current_device() {
     c->device = dev;
     AGPM_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev));
     AGPM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    AGPM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = ~0ull;  // never trim: freed graph memory stays cached for the next view
+    AGPM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     g_ctx[dev] = c;
   }
   return *g_ctx[dev];
@@ -125,11 +143,11 @@ void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsig
                    cudaStream_t s) {
   const uint32_t n = g->n;
   DeviceCtx& ctx = ctx_for_current_device();
-  AGPM_CUDA(cudaMalloc(&g->vtx, sizeof(VtxInfo) * (size_t)(n ? n : 1)));
+  AGPM_CUDA(dev_malloc(&g->vtx, sizeof(VtxInfo) * (size_t)(n ? n : 1)));
   unsigned long long* deg = nullptr;
   unsigned long long* prefix = nullptr;
-  AGPM_CUDA(cudaMalloc(&deg, sizeof(unsigned long long) * ((size_t)n + 1)));
-  AGPM_CUDA(cudaMalloc(&prefix, sizeof(unsigned long long) * ((size_t)n + 1)));
+  AGPM_CUDA(dev_malloc(&deg, sizeof(unsigned long long) * ((size_t)n + 1)));
+  AGPM_CUDA(dev_malloc(&prefix, sizeof(unsigned long long) * ((size_t)n + 1)));
   int blocks = ctx.sm_count * 8;
   if (n) {
     vtx_kernel<<<blocks, 256, 0, s>>>(d_begin, d_end, g->nbr, n, g->vtx, deg);
@@ -142,7 +160,7 @@ void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsig
   cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, deg, prefix + 1, (int64_t)n, s);
   size_t tmp_bytes2 = 0;
   unsigned long long* red = nullptr;
-  AGPM_CUDA(cudaMalloc(&red, sizeof(unsigned long long)));
+  AGPM_CUDA(dev_malloc(&red, sizeof(unsigned long long)));
   cub::DeviceReduce::Max(nullptr, tmp_bytes2, deg, red, (int64_t)n + 1, s);
   void* tmp = ctx.get(7, std::max(tmp_bytes, tmp_bytes2) + 16);
   if (n) {
@@ -155,16 +173,16 @@ void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsig
   AGPM_CUDA(cudaStreamSynchronize(s));
   g->arcs = arcs;
   g->max_degree = maxd;
-  AGPM_CUDA(cudaMalloc(&g->seed_arcs, sizeof(unsigned long long) * (size_t)(arcs ? arcs : 1)));
+  AGPM_CUDA(dev_malloc(&g->seed_arcs, sizeof(unsigned long long) * (size_t)(arcs ? arcs : 1)));
   if (n && arcs) {
     seed_arcs_kernel<<<blocks, 256, 0, s>>>(g->vtx, g->nbr, prefix, n, g->seed_arcs);
     count_launch();
     AGPM_CUDA(cudaGetLastError());
   }
   AGPM_CUDA(cudaStreamSynchronize(s));
-  AGPM_CUDA(cudaFree(deg));
-  AGPM_CUDA(cudaFree(prefix));
-  AGPM_CUDA(cudaFree(red));
+  AGPM_CUDA(dev_free(deg));
+  AGPM_CUDA(dev_free(prefix));
+  AGPM_CUDA(dev_free(red));
   g->bytes = sizeof(VtxInfo) * (uint64_t)n + 4ull * g->nbr_len + 8ull * arcs;
 }
 
@@ -210,10 +228,10 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
     g->plain = end == nullptr && begin[0] == 0;
     unsigned long long *d_begin = nullptr, *d_end = nullptr;
     size_t nb = end ? n : (size_t)n + 1;
-    AGPM_CUDA(cudaMalloc(&d_begin, sizeof(uint64_t) * (nb ? nb : 1)));
+    AGPM_CUDA(dev_malloc(&d_begin, sizeof(uint64_t) * (nb ? nb : 1)));
     AGPM_CUDA(cudaMemcpyAsync(d_begin, begin, sizeof(uint64_t) * nb, cudaMemcpyHostToDevice, s));
     if (end) {
-      AGPM_CUDA(cudaMalloc(&d_end, sizeof(uint64_t) * (n ? n : 1)));
+      AGPM_CUDA(dev_malloc(&d_end, sizeof(uint64_t) * (n ? n : 1)));
       AGPM_CUDA(cudaMemcpyAsync(d_end, end, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s));
     }
     g->nbr = alloc_nbr(neighbor_len, s);
@@ -221,8 +239,8 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
       AGPM_CUDA(cudaMemcpyAsync(g->nbr, neighbors, sizeof(uint32_t) * neighbor_len,
                                 cudaMemcpyHostToDevice, s));
     finalize_view(g, d_begin, d_end, s);
-    AGPM_CUDA(cudaFree(d_begin));
-    if (d_end) AGPM_CUDA(cudaFree(d_end));
+    AGPM_CUDA(dev_free(d_begin));
+    if (d_end) AGPM_CUDA(dev_free(d_end));
     *out = g;
   });
 }
@@ -230,11 +248,11 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
 int agpm_graph_free(agpm_graph* g) {
   return guarded([&] {
     if (!g) return;
-    cudaFree(g->vtx);
-    cudaFree(g->nbr);
-    cudaFree(g->seed_arcs);
-    if (g->ehash) cudaFree(g->ehash);
-    if (g->core) cudaFree(g->core);
+    dev_free(g->vtx);
+    dev_free(g->nbr);
+    dev_free(g->seed_arcs);
+    if (g->ehash) dev_free(g->ehash);
+    if (g->core) dev_free(g->core);
     delete g;
   });
 }

@@ -43,7 +43,7 @@ void ensure_edge_hash(agpm_graph* g, cudaStream_t s) {
   for (int attempt = 0; attempt < 4; ++attempt, buckets <<= 1) {
     if (buckets > (1ull << 32)) throw std::invalid_argument("edge hash: too many edges");
     unsigned long long* table = nullptr;
-    AGPM_CUDA(cudaMalloc(&table, 32ull * buckets));
+    AGPM_CUDA(dev_malloc(&table, 32ull * buckets));
     AGPM_CUDA(cudaMemsetAsync(table, 0xff, 32ull * buckets, s));
     AGPM_CUDA(cudaMemsetAsync(overflow, 0, 4, s));
     const unsigned blocks = (unsigned)std::min<unsigned long long>((g->arcs + 255) / 256, (unsigned long long)ctx.sm_count * 16);
@@ -62,7 +62,7 @@ void ensure_edge_hash(agpm_graph* g, cudaStream_t s) {
       g->bytes += 32ull * buckets;
       return;
     }
-    AGPM_CUDA(cudaFree(table));
+    AGPM_CUDA(dev_free(table));
   }
   throw cuda_error("edge hash build kept overflowing");
 }

@@ -42,10 +42,10 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    AGPM_CUDA(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
+    AGPM_CUDA(dev_malloc(&p, sizeof(T) * (count ? count : 1)));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p);
     p = nullptr;
     n = 0;
   }
@@ -328,26 +328,26 @@ agpm_graph* view_from_sorted_arcs(DevBuf<unsigned long long>& arcs, uint64_t cou
       AGPM_CUDA(cub::DeviceScan::InclusiveSum(t.p, t1, last.p, begin.p + 1, (int64_t)n, s));
       AGPM_CUDA(cub::DeviceReduce::Max(t.p, t2, last.p, red.p, (int64_t)n, s));
       AGPM_CUDA(cudaMemcpyAsync(&maxd, red.p, 8, cudaMemcpyDeviceToHost, s));
-      AGPM_CUDA(cudaMalloc(&g->vtx, sizeof(VtxInfo) * (size_t)n));
+      AGPM_CUDA(dev_malloc(&g->vtx, sizeof(VtxInfo) * (size_t)n));
       vtx_from_bounds_kernel<<<grid_for(n, sm), 256, 0, s>>>(begin.p, g->nbr, n, g->vtx);
       count_launch();
       AGPM_CUDA(cudaGetLastError());
       AGPM_CUDA(cudaStreamSynchronize(s));
     } else {
-      AGPM_CUDA(cudaMalloc(&g->vtx, sizeof(VtxInfo)));
+      AGPM_CUDA(dev_malloc(&g->vtx, sizeof(VtxInfo)));
     }
     g->max_degree = maxd;
     if (count) {
       g->seed_arcs = arcs.take();
     } else {
-      AGPM_CUDA(cudaMalloc(&g->seed_arcs, 8));
+      AGPM_CUDA(dev_malloc(&g->seed_arcs, 8));
     }
     g->bytes = sizeof(VtxInfo) * (uint64_t)n + 4ull * g->nbr_len + 8ull * g->arcs;
     return g;
   } catch (...) {
-    cudaFree(g->vtx);
-    cudaFree(g->nbr);
-    cudaFree(g->seed_arcs);
+    dev_free(g->vtx);
+    dev_free(g->nbr);
+    dev_free(g->seed_arcs);
     delete g;
     throw;
   }

@@ -117,7 +117,7 @@ agpm_graph* induced_suffix_device(const agpm_graph* g, uint32_t lo, cudaStream_t
   DeviceCtx& ctx = ctx_for_current_device();
   const uint32_t n = g->n;
   unsigned long long* offs = nullptr;
-  AGPM_CUDA(cudaMalloc(&offs, 8ull * ((size_t)n + 1)));
+  AGPM_CUDA(dev_malloc(&offs, 8ull * ((size_t)n + 1)));
   AGPM_CUDA(cudaMemsetAsync(offs + n, 0, 8, s));
   if (n) {
     induced_count_kernel<<<grid(n), 256, 0, s>>>(g->vtx, g->nbr, n, lo, offs);
@@ -145,7 +145,7 @@ agpm_graph* induced_suffix_device(const agpm_graph* g, uint32_t lo, cudaStream_t
     AGPM_CUDA(cudaGetLastError());
   }
   finalize_view(out, offs, nullptr, s);
-  AGPM_CUDA(cudaFree(offs));
+  AGPM_CUDA(dev_free(offs));
   return out;
 }
 

@@ -127,9 +127,9 @@ agpm_graph* color_split_device(const agpm_graph* g, uint32_t c, uint64_t seed, u
   out->oriented = false;
   uint32_t* colors = nullptr;
   unsigned long long *begin = nullptr, *split = nullptr;
-  AGPM_CUDA(cudaMalloc(&colors, 4ull * (n ? n : 1)));
-  AGPM_CUDA(cudaMalloc(&begin, 8ull * (n ? n : 1)));
-  AGPM_CUDA(cudaMalloc(&split, 8ull * (n ? n : 1)));
+  AGPM_CUDA(dev_malloc(&colors, 4ull * (n ? n : 1)));
+  AGPM_CUDA(dev_malloc(&begin, 8ull * (n ? n : 1)));
+  AGPM_CUDA(dev_malloc(&split, 8ull * (n ? n : 1)));
   out->nbr = alloc_nbr(g->nbr_len, s);
   auto* tot = static_cast<unsigned long long*>(ctx.get(3, 64));
   AGPM_CUDA(cudaMemsetAsync(tot, 0, 8, s));
@@ -146,9 +146,9 @@ agpm_graph* color_split_device(const agpm_graph* g, uint32_t c, uint64_t seed, u
   out->edge_count = same / 2;  // same_color_edge_count (colored_csr.cpp:45)
   if (same_edges) *same_edges = same / 2;
   finalize_view(out, begin, split, s);
-  AGPM_CUDA(cudaFree(colors));
-  AGPM_CUDA(cudaFree(begin));
-  AGPM_CUDA(cudaFree(split));
+  AGPM_CUDA(dev_free(colors));
+  AGPM_CUDA(dev_free(begin));
+  AGPM_CUDA(dev_free(split));
   return out;
 }
 
@@ -157,7 +157,7 @@ agpm_graph* bernoulli_device(const agpm_graph* g, double p, uint64_t seed, cudaS
   DeviceCtx& ctx = ctx_for_current_device();
   const uint32_t n = g->n;
   unsigned long long* offs = nullptr;
-  AGPM_CUDA(cudaMalloc(&offs, 8ull * ((size_t)n + 1)));
+  AGPM_CUDA(dev_malloc(&offs, 8ull * ((size_t)n + 1)));
   AGPM_CUDA(cudaMemsetAsync(offs + n, 0, 8, s));
   if (n) {
     bern_count_kernel<<<grid_for(n), 256, 0, s>>>(g->vtx, g->nbr, n, seed, p, offs);
@@ -184,7 +184,7 @@ agpm_graph* bernoulli_device(const agpm_graph* g, double p, uint64_t seed, cudaS
     AGPM_CUDA(cudaGetLastError());
   }
   finalize_view(out, offs, nullptr, s);
-  AGPM_CUDA(cudaFree(offs));
+  AGPM_CUDA(dev_free(offs));
   return out;
 }
 
