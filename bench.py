@@ -265,7 +265,7 @@ def run_gpu(args):
     value = B * world * args.steps / (ms / 1000.0)
 
     # ---- e2e through the public C-ABI with host buffers (graph upload + fixed budget + read-back)
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(1, args.steps)  # every timed step, so a single slow host hiccup is amortised like in `value`
     g.pin()  # inputs come from pinned host memory
     h2d = int(off.nbytes + nbr.nbytes)
     d2h = int(((B + 4095) // 4096) * 32)
