@@ -242,18 +242,19 @@ def run_gpu(args):
     k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = A.kernel_launches()
-    with Clocks(torch.cuda.current_device()) as clk:
-        ev0.record(stream)
-        for s in range(args.steps):
-            first = (s * world + rank) * B
-            k_start[s].record(stream)
-            A.sample_dev(dg, plan, 1, first, B, values.data_ptr(), sptr)
-            k_end[s].record(stream)
-            A.window_moments_dev(values.data_ptr(), B, WINDOW, wins.data_ptr(), sptr)
-            if dist is not None:
-                dist.all_gather_into_tensor(gathered, wins)
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    # clocks sampled over both timed regions (device-resident steps, then e2e steps)
+    clk = Clocks(torch.cuda.current_device()).__enter__()
+    ev0.record(stream)
+    for s in range(args.steps):
+        first = (s * world + rank) * B
+        k_start[s].record(stream)
+        A.sample_dev(dg, plan, 1, first, B, values.data_ptr(), sptr)
+        k_end[s].record(stream)
+        A.window_moments_dev(values.data_ptr(), B, WINDOW, wins.data_ptr(), sptr)
+        if dist is not None:
+            dist.all_gather_into_tensor(gathered, wins)
+    ev1.record(stream)
+    torch.cuda.synchronize()
     launches = A.kernel_launches() - launches0
     ms = ev0.elapsed_time(ev1)
     kern_ms = sum(a.elapsed_time(b) for a, b in zip(k_start, k_end)) / args.steps
@@ -296,6 +297,7 @@ def run_gpu(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e_value = B * world * e2e_steps / e2e_s
+    clk.__exit__(None, None, None)
 
     # ---- time to converge (1%@95%) on the resident graph, rank 0's device
     ttc = None
