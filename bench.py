@@ -301,7 +301,43 @@ def run_gpu(args):
 
     # ---- time to converge (1%@95%) on the resident graph, rank 0's device
     ttc = None
-    if rank == 0:
+    if world > 1:
+        # sharded run_ns_online (distributed.py): ids sharded by rank, window
+        # moments all-gathered over NCCL each batch, every rank replays the
+        # reference's window loop; wall time is the max over ranks
+        from paper_2405_03488_b200.distributed import run_ns_online_sharded
+
+        per_rank = max(WINDOW, ((1 << 19) // world // WINDOW) * WINDOW)
+        nw_b = per_rank // WINDOW
+        v_b = torch.empty(per_rank, dtype=torch.float64, device=dev)
+        w_b = torch.empty((nw_b, 4), dtype=torch.float64, device=dev)
+        g_b = torch.empty((world * nw_b, 4), dtype=torch.float64, device=dev)
+
+        def sample_moments(first, count):
+            A.sample_dev(dg, plan, 1, first, count, v_b.data_ptr(), sptr)
+            A.window_moments_dev(v_b.data_ptr(), count, WINDOW, w_b.data_ptr(), sptr)
+            torch.cuda.synchronize()
+            return w_b[: (count + WINDOW - 1) // WINDOW].cpu().numpy()
+
+        def all_gather(local):
+            w_b.copy_(torch.from_numpy(local))
+            dist.all_gather_into_tensor(g_b, w_b)
+            return g_b.cpu().numpy()
+
+        for rep in range(2):  # first run warms the path
+            dist.barrier()
+            torch.cuda.synchronize()
+            t_on = time.perf_counter()
+            mg = run_ns_online_sharded(sample_moments, all_gather, rank, world, 0.01, 0.05, window=WINDOW,
+                                       per_rank=per_rank)
+            torch.cuda.synchronize()
+            tt = torch.tensor([time.perf_counter() - t_on], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        rp = mg.report
+        ttc = {"seconds": float(tt.item()), "samples": rp.n, "windows": mg.windows, "estimate": rp.mu,
+               "epsilon_hat": rp.epsilon_hat, "hit_rate": rp.hit_rate, "converged": bool(rp.converged),
+               "ranks": world, "samples_per_rank_per_batch": per_rank}
+    elif rank == 0:
         A.run_ns_online(dg, plan, 0.01, 0.05, A.OnlinePolicy(), seed=1)
         r = A.run_ns_online(dg, plan, 0.01, 0.05, A.OnlinePolicy(), seed=1)
         ttc = {"seconds": r.seconds, "samples": r.report.n, "windows": r.windows,
