@@ -228,7 +228,7 @@ int agpm_ns_set_strategy(int strategy);
 int agpm_ns_set_frontier_reuse(int on);
 /* frontier only: dimension C of the dense-core adjacency bit matrix (top C ids,
  * C*C/8 bytes, kept in L2) that answers core-core membership tests in one
- * load; 0 disables; default 32768. Results are identical either way. */
+ * load; 0 disables; default 65536. Results are identical either way. */
 int agpm_ns_set_core_dim(uint32_t dim);
 
 /* Device-pointer building blocks (bench / multi-rank driver): enqueue only.
@@ -249,6 +249,12 @@ int agpm_ns_bmin_bytes(agpm_graph* g, const agpm_plan* plan, uint64_t seed, uint
  * skip the order bounds (every arc is a seed), symmetric views apply them and
  * skip u > v seeds when the plan orients the seed edge. */
 int agpm_exact_count(agpm_graph* g, const agpm_plan* plan, uint64_t* count, void* stream);
+/* One shard of agpm_exact_count for multi-GPU counting: shard r of
+ * nshards counts the seeds of 32-arc chunks r, r + nshards, ... (interleaved
+ * over the arc array, so hub-heavy ranges spread over the ranks); the shards'
+ * counts sum to agpm_exact_count. Ranks all-reduce the u64 partial counts. */
+int agpm_exact_count_shard(agpm_graph* g, const agpm_plan* plan, uint32_t shard, uint32_t nshards,
+                           uint64_t* count, void* stream);
 
 /* ------------------------------------------- sparsification and GS -------
  * colour split: ColoredCsr::color_vertices (colored_csr.cpp:48-54) -> the

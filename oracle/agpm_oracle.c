@@ -557,9 +557,12 @@ static uint64_t dfs(const view_t* g, const agpm_plan* plan, int apply_bounds, ui
   return count;
 }
 
-int orc_exact_count(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t* end,
-                    const uint32_t* nbr, int oriented, const agpm_plan* plan, uint64_t* count) {
-  /* exact_engine.cpp:66-91 */
+/* exact_engine.cpp:66-91, restricted to the seeds of one shard: arc index idx
+ * (u ascending, list order — the device's seed-arc order) belongs to shard
+ * (idx / 32) % nshards. nshards = 1 is the reference's exact_count. */
+int orc_exact_count_shard(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t* end,
+                          const uint32_t* nbr, int oriented, const agpm_plan* plan, uint32_t shard,
+                          uint32_t nshards, uint64_t* count) {
   view_t g = mkview(n, m, begin, end, nbr, oriented);
   int is_clique = plan->n_edges == plan->k * (plan->k - 1) / 2;
   int oriented_clique = oriented && is_clique;
@@ -569,10 +572,12 @@ int orc_exact_count(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_
   scratch_t frames[AGPM_MAX_K];
   memset(frames, 0, sizeof(frames));
   uint32_t binding[AGPM_MAX_K];
-  uint64_t total = 0;
+  if (nshards == 0 || shard >= nshards) return AGPM_E_INVALID;
+  uint64_t total = 0, idx = 0;
   for (uint32_t u = 0; u < n; ++u) {
-    for (uint64_t e = g.begin[u]; e < g.end[u]; ++e) {
+    for (uint64_t e = g.begin[u]; e < g.end[u]; ++e, ++idx) {
       uint32_t v = g.nbr[e];
+      if ((idx / 32) % nshards != shard) continue;
       if (!oriented_clique && plan->seed_ordered && u > v) continue;
       binding[0] = u;
       binding[1] = v;
@@ -590,6 +595,11 @@ int orc_exact_count(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_
   }
   *count = total;
   return AGPM_OK;
+}
+
+int orc_exact_count(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t* end,
+                    const uint32_t* nbr, int oriented, const agpm_plan* plan, uint64_t* count) {
+  return orc_exact_count_shard(n, m, begin, end, nbr, oriented, plan, 0, 1, count);
 }
 
 /* ------------------------------------------------------------ csr_graph.cpp:172-239 */

@@ -28,7 +28,7 @@ __all__ = [
     "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
     "hit_rate_report", "exact_count", "exact_count_rooted", "region_split", "gs_estimate", "choose_keep_probability", "ns_cost_cone",
     "gs_cost_estimate", "select_scheme", "count_matches_through_edge", "estimate_gamma", "fast_profile",
-    "calibrate_hardware_constant", "count_hybrid", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "calibrate_hardware_constant", "count_hybrid", "exact_count_shard", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
 ]
 
@@ -130,6 +130,7 @@ def _declare(L):
         "agpm_ns_bmin_bytes": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pu64, A.P]),
         "agpm_ns_set_strategy": (C.c_int, [C.c_int]),
         "agpm_exact_count": (C.c_int, [A.P, A.pPlan, A.pu64, A.P]),
+        "agpm_exact_count_shard": (C.c_int, [A.P, A.pPlan, A.u32, A.u32, A.pu64, A.P]),
         "agpm_color_split": (C.c_int, [A.P, A.u32, A.u64, A.pu32, A.pu64, C.POINTER(A.P), A.P]),
         "agpm_bernoulli_sparsify": (C.c_int, [A.P, C.c_double, A.u64, C.POINTER(A.P), A.P]),
         "agpm_gs_estimate": (C.c_int, [A.P, A.pPlan, C.c_int, C.c_double, A.u32, A.u64, C.POINTER(A.GsResult), A.P]),
@@ -476,6 +477,14 @@ def exact_count(dg, plan, threads=1, stream=None):
     return out.value
 
 
+def exact_count_shard(dg, plan, shard, nshards, stream=None):
+    """One rank's share of exact_count: seeds of 32-arc chunks shard, shard + nshards, ...
+    The shards sum to exact_count (all-reduce the partials across ranks)."""
+    out = C.c_uint64()
+    _check(lib().agpm_exact_count_shard(dg._h, C.byref(plan), shard, nshards, C.byref(out), stream))
+    return out.value
+
+
 def gs_estimate(dg, plan, scheme="color", keep_probability=1.0, colors=1, seed=0, threads=1, stream=None):
     """gs_estimate (gs_engine.cpp:42-75): scheme "color" (scale c^(k-1)) or "bernoulli" (scale p^-l)."""
     out = _abi.GsResult()
@@ -592,7 +601,7 @@ def set_strategy(name):
 
 
 def set_core_dim(dim):
-    """Dense-core bit-matrix dimension for the frontier sampler (0 = off, default 32768)."""
+    """Dense-core bit-matrix dimension for the frontier sampler (0 = off, default 65536)."""
     _check(lib().agpm_ns_set_core_dim(int(dim)))
 
 

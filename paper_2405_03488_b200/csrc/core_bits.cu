@@ -4,12 +4,14 @@
 // vertices, and eager-verify candidates always sit above the bound vertices'
 // ids for clique-like steps — so most membership tests "a in N(w)" of the
 // intersection phase have both a and w among the top ids. For the top C ids
-// (the "core", default C = 32768 -> a 128 MB matrix; its hot rows stay in the 126 MB L2)
+// (the "core", default C = 65536 -> a 512 MB matrix; its hot rows stay in the 126 MB L2)
 // the adjacency is kept as a C x C bit matrix: a core test is ONE L2 word load
 // per lane instead of a splitter load, a shuffle search and a dependent
 // per-lane search. On config 2, 92 % / 97.7 % of the isect membership tests
 // fall inside a 16 K / 32 K core, and one 2^24-sample 4-clique launch drops
-// from 27.2 ms to 15.9 ms (profiles/r1/README.md).
+// from 27.2 ms to 15.9 ms (profiles/r1/README.md). With the flat sampler a
+// 64 K core beats 32 K on every RMAT scale measured (20: 8.8 vs 9.4 ms, 22:
+// 15.1 vs 17.0, 24: 26.4 vs 36.2, 27: 79.5 vs 91.8 ms per 2^24 4-clique samples).
 //
 // Exact by construction (it is the adjacency restricted to [base, n)), so it
 // changes no result; it only replaces how membership is answered.
@@ -21,7 +23,7 @@
 namespace agpm_b200 {
 namespace {
 
-uint32_t g_core_dim = 32768;
+uint32_t g_core_dim = 65536;
 
 // one warp per core row: build the row in shared memory, then write it out
 __global__ void __launch_bounds__(256) core_rows_kernel(const VtxInfo* __restrict__ vtx,
@@ -52,6 +54,7 @@ __global__ void __launch_bounds__(256) core_rows_kernel(const VtxInfo* __restric
 }  // namespace
 
 void set_core_dim(uint32_t dim) { g_core_dim = dim; }
+uint32_t core_dim_setting() { return g_core_dim; }
 
 void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
   const uint32_t want = g->oriented || !g->plain ? 0u : std::min(g_core_dim, g->n);

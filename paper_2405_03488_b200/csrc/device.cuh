@@ -95,4 +95,9 @@ void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsig
 void ensure_edge_hash(agpm_graph* g, cudaStream_t s);
 // build (or drop, when the configured dimension is 0) g->core for the current core dimension
 void ensure_core_bits(agpm_graph* g, cudaStream_t s);
+uint32_t core_dim_setting();
+// exact_count (exact_engine.cpp:66-91) on the device; root_limit keeps seeds whose
+// first vertex is below it, shard/nshards keep every nshards-th 32-arc chunk
+unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan, cudaStream_t s,
+                                      uint32_t root_limit = 0xffffffffu, uint32_t shard = 0, uint32_t nshards = 1);
 }  // namespace agpm_b200

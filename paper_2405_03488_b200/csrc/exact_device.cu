@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(256) exact_kernel(const GraphArgs g, const Dev
                                                     const int skip_unordered, const uint32_t root_limit,
                                                     uint32_t* __restrict__ scratch,
                                                     const uint32_t cap, unsigned long long* __restrict__ cursor,
-                                                    unsigned long long* __restrict__ count_out) {
+                                                    unsigned long long* __restrict__ count_out,
+                                                    const uint32_t shard, const uint32_t nshards) {
   constexpr int L = K - 2;  // steps
   const int lane = threadIdx.x & 31;
   const unsigned long long gw = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
@@ -89,7 +90,9 @@ __global__ void __launch_bounds__(256) exact_kernel(const GraphArgs g, const Dev
   for (;;) {
     if (next >= end) {
       unsigned long long b = 0;
-      if (lane == 0) b = atomicAdd(cursor, 32ull);
+      // 32-arc chunks handed out dynamically; shard r of N owns chunks r, r+N, ...
+      // (interleaved, so hub-heavy arc ranges spread over the ranks)
+      if (lane == 0) b = (atomicAdd(cursor, 1ull) * nshards + shard) * 32ull;
       b = __shfl_sync(FULL, b, 0);
       if (b >= g.arcs) break;
       next = b;
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(256) exact_kernel(const GraphArgs g, const Dev
 
 template <int K>
 unsigned long long run_exact_k(const agpm_graph* gr, const DevPlan& p, bool apply_bounds, bool skip_unordered,
-                               uint32_t root_limit, cudaStream_t s) {
+                               uint32_t root_limit, uint32_t shard, uint32_t nshards, cudaStream_t s) {
   DeviceCtx& ctx = ctx_for_current_device();
   GraphArgs g{gr->vtx, gr->nbr, gr->seed_arcs, gr->arcs, gr->plain, nullptr, 0};
   int occ = 0;
@@ -258,7 +261,7 @@ unsigned long long run_exact_k(const agpm_graph* gr, const DevPlan& p, bool appl
   auto* cnt = static_cast<unsigned long long*>(ctx.get(3, 64));
   AGPM_CUDA(cudaMemsetAsync(cnt, 0, 16, s));
   exact_kernel<K><<<blocks, 256, 0, s>>>(g, p, apply_bounds ? 1 : 0, skip_unordered ? 1 : 0, root_limit, scratch,
-                                         cap, cnt, cnt + 1);
+                                         cap, cnt, cnt + 1, shard, nshards);
   count_launch();
   AGPM_CUDA(cudaGetLastError());
   unsigned long long h = 0;
@@ -272,7 +275,8 @@ unsigned long long run_exact_k(const agpm_graph* gr, const DevPlan& p, bool appl
 // exact_count (exact_engine.cpp:66-91), eager plans; root_limit keeps only
 // seeds whose first vertex is below it (region split)
 unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan, cudaStream_t s,
-                                      uint32_t root_limit) {
+                                      uint32_t root_limit, uint32_t shard, uint32_t nshards) {
+  if (nshards == 0 || shard >= nshards) throw std::invalid_argument("shard must be < nshards");
   if (!plan || plan->k < 2 || plan->k > AGPM_MAX_K || plan->n_steps != plan->k - 2)
     throw std::invalid_argument("malformed plan");
   const bool clique = plan->n_edges == plan->k * (plan->k - 1) / 2;
@@ -283,8 +287,8 @@ unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan
   const bool oriented_clique = g->oriented && clique;
   const bool apply_bounds = !oriented_clique;
   const bool skip_unordered = !oriented_clique && plan->seed_ordered;
-  if (plan->k == 2 && root_limit == 0xffffffffu)
-    return skip_unordered ? g->arcs / 2 : g->arcs;  // every (ordered) arc is a match
+  if (plan->k == 2 && root_limit == 0xffffffffu)  // every (ordered) arc is a match; shard 0 reports it
+    return shard ? 0ull : skip_unordered ? g->arcs / 2 : g->arcs;
   DevPlan d{};
   d.k = plan->k;
   d.n_steps = plan->n_steps;
@@ -303,13 +307,13 @@ unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan
   }
   if (g->arcs == 0) return 0;
   switch (plan->k) {
-    case 3: return run_exact_k<3>(g, d, apply_bounds, skip_unordered, root_limit, s);
-    case 4: return run_exact_k<4>(g, d, apply_bounds, skip_unordered, root_limit, s);
-    case 5: return run_exact_k<5>(g, d, apply_bounds, skip_unordered, root_limit, s);
-    case 6: return run_exact_k<6>(g, d, apply_bounds, skip_unordered, root_limit, s);
-    case 7: return run_exact_k<7>(g, d, apply_bounds, skip_unordered, root_limit, s);
-    case 8: return run_exact_k<8>(g, d, apply_bounds, skip_unordered, root_limit, s);
-    case 9: return run_exact_k<9>(g, d, apply_bounds, skip_unordered, root_limit, s);
+    case 3: return run_exact_k<3>(g, d, apply_bounds, skip_unordered, root_limit, shard, nshards, s);
+    case 4: return run_exact_k<4>(g, d, apply_bounds, skip_unordered, root_limit, shard, nshards, s);
+    case 5: return run_exact_k<5>(g, d, apply_bounds, skip_unordered, root_limit, shard, nshards, s);
+    case 6: return run_exact_k<6>(g, d, apply_bounds, skip_unordered, root_limit, shard, nshards, s);
+    case 7: return run_exact_k<7>(g, d, apply_bounds, skip_unordered, root_limit, shard, nshards, s);
+    case 8: return run_exact_k<8>(g, d, apply_bounds, skip_unordered, root_limit, shard, nshards, s);
+    case 9: return run_exact_k<9>(g, d, apply_bounds, skip_unordered, root_limit, shard, nshards, s);
     case 2: throw std::invalid_argument("rooted counts of a single edge are not supported");
     default: throw std::invalid_argument("device exact counter needs 2 <= k <= 9");
   }
@@ -320,7 +324,15 @@ unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan
 extern "C" int agpm_exact_count(agpm_graph* g, const agpm_plan* plan, uint64_t* count, void* stream) {
   return agpm_b200::guarded([&] {
     if (!g || !count) throw std::invalid_argument("null argument");
-    *count = agpm_b200::exact_count_device(g, plan, agpm_b200::pick_stream(stream), 0xffffffffu);
+    *count = agpm_b200::exact_count_device(g, plan, agpm_b200::pick_stream(stream), 0xffffffffu, 0, 1);
+  });
+}
+
+extern "C" int agpm_exact_count_shard(agpm_graph* g, const agpm_plan* plan, uint32_t shard, uint32_t nshards,
+                                      uint64_t* count, void* stream) {
+  return agpm_b200::guarded([&] {
+    if (!g || !count) throw std::invalid_argument("null argument");
+    *count = agpm_b200::exact_count_device(g, plan, agpm_b200::pick_stream(stream), 0xffffffffu, shard, nshards);
   });
 }
 
@@ -328,6 +340,6 @@ extern "C" int agpm_exact_count_rooted(agpm_graph* g, const agpm_plan* plan, uin
                                        void* stream) {
   return agpm_b200::guarded([&] {
     if (!g || !count) throw std::invalid_argument("null argument");
-    *count = agpm_b200::exact_count_device(g, plan, agpm_b200::pick_stream(stream), root_limit);
+    *count = agpm_b200::exact_count_device(g, plan, agpm_b200::pick_stream(stream), root_limit, 0, 1);
   });
 }

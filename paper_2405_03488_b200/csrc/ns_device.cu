@@ -190,11 +190,14 @@ GraphArgs graph_args(const agpm_graph* g) {
 constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3, kStrategyFused = 4, kStrategyFlat = 5;
 int g_strategy = kStrategyAuto;
 
-// clique plans (every step intersects all bound vertices' lists, no out-lists):
-// their drivers are short suffixes answered by the dense core, where the flat
-// sampler wins (config 2, per 2^24 samples: triangle 6.2 vs 7.8 ms, 4-clique
-// 9.3 vs 12.8, 5-clique 14.7 vs 18.3); elsewhere (4-cycle 10.9 vs 9.9, house
-// 170 vs 82) long non-core drivers favour the frontier phases
+// clique plans (every step intersects all bound vertices' lists, no out-lists)
+// on graphs whose dense core is a large enough slice (n <= 64 x core dim): their
+// drivers are short suffixes answered by the core, where the flat sampler wins
+// (config-2 graph, per 2^24 samples: triangle 6.2 vs 7.8 ms, 4-clique 8.8 vs
+// 12.5, 5-clique 14.1 vs 18.1; RMAT-22 4-clique 15.1 vs 16.1). Beyond that
+// (RMAT-24: 26.4 vs 22.2 ms, RMAT-27: 79.5 vs 47.2 ms) and for non-clique plans
+// (4-cycle 10.9 vs 9.9 ms, house 170 vs 82) long non-core drivers favour the
+// frontier phases.
 bool clique_plan(const DevPlan& p) {
   for (int s = 0; s < p.k - 2; ++s)
     if (p.in_mask[s] != (1u << (s + 2)) - 1u || p.out_mask[s] != 0) return false;
@@ -203,7 +206,8 @@ bool clique_plan(const DevPlan& p) {
 
 int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count) {
   if (g_strategy != kStrategyAuto) return g_strategy;
-  if (count >= (1ull << 18) && clique_plan(p)) return kStrategyFlat;
+  const uint64_t core = core_dim_setting();
+  if (count >= (1ull << 18) && clique_plan(p) && core && g->n <= 64 * core) return kStrategyFlat;
   const double avg_deg = g->n ? static_cast<double>(g->arcs) / g->n : 0.0;
   if (avg_deg <= 24.0 && g->max_degree <= 256) return kStrategyLane;
   return count >= (1ull << 18) ? kStrategyFrontier : kStrategyWarp;

@@ -17,9 +17,6 @@
 
 namespace agpm_b200 {
 
-unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan, cudaStream_t s,
-                                      uint32_t root_limit = 0xffffffffu);
-
 namespace {
 
 constexpr unsigned FULLM = 0xffffffffu;

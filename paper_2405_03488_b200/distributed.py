@@ -16,7 +16,7 @@ import numpy as np
 
 from ._abi import Accumulator, Report
 
-__all__ = ["predicted_error_py", "WindowMerger", "batch_first_id", "run_ns_online_sharded"]
+__all__ = ["predicted_error_py", "WindowMerger", "batch_first_id", "run_ns_online_sharded", "exact_count_sharded"]
 
 
 def _inv_norm_cdf(q):
@@ -150,3 +150,14 @@ def run_ns_online_sharded(sample_moments, all_gather, rank, world, eps, delta, w
         merger.feed(all_gather(local))
         batch += 1
     return merger
+
+
+def exact_count_sharded(count_shard, all_reduce_sum, rank, world):
+    """Multi-rank exact_count: every rank holds the whole graph,
+    counts the seeds of its interleaved 32-arc chunks (count_shard(rank, world),
+    e.g. agpm.exact_count_shard on its own GPU) and the u64 partials are summed
+    across ranks (NCCL all-reduce on GPUs, gloo in the CPU tests). Returns the
+    total on every rank; it equals the single-GPU exact_count exactly."""
+    if not (0 <= rank < world):
+        raise ValueError("rank must be in [0, world)")
+    return int(all_reduce_sum(int(count_shard(rank, world))))

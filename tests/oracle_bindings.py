@@ -65,6 +65,7 @@ class Oracle:
             "orc_ns_online": (C.c_int, graph + [pPlan, dbl, dbl, C.POINTER(OnlinePolicy), u64,
                                                 C.POINTER(OnlineResult)]),
             "orc_exact_count": (C.c_int, graph + [C.c_int, pPlan, pu64]),
+            "orc_exact_count_shard": (C.c_int, graph + [C.c_int, pPlan, u32, u32, pu64]),
             "orc_orient_by_degree": (None, [u32, pu64, pu32, pu64, pu32]),
             "orc_bernoulli_sparsify": (u64, [u32, pu64, pu32, dbl, u64, pu64, pu32]),
             "orc_triangle_count": (u64, [u32, pu64, pu32]),
@@ -138,6 +139,15 @@ class Oracle:
         keep, (n, po, pe, pn) = self._g(off, nbr, end)
         out = C.c_uint64()
         st = self.L.orc_exact_count(n, m, po, pe, pn, int(oriented), C.byref(plan), C.byref(out))
+        if st != 0:
+            raise ValueError("invalid exact_count arguments")
+        return out.value
+
+    def exact_count_shard(self, off, nbr, m, plan, shard, nshards, oriented=False, end=None):
+        keep, (n, po, pe, pn) = self._g(off, nbr, end)
+        out = C.c_uint64()
+        st = self.L.orc_exact_count_shard(n, m, po, pe, pn, int(oriented), C.byref(plan), shard, nshards,
+                                          C.byref(out))
         if st != 0:
             raise ValueError("invalid exact_count arguments")
         return out.value

@@ -82,3 +82,25 @@ def test_exact_errors(agpm):
         agpm.exact_count(og, agpm.compile_plan("5path"))  # non-clique on oriented input
     with pytest.raises(ValueError):
         agpm.exact_count(agpm.DeviceGraph(g), agpm.compile_plan("4clique", "lazy"))
+
+
+@pytest.mark.parametrize("nshards", [2, 3, 8])
+@pytest.mark.parametrize("pattern", ["triangle", "4clique", "4cycle", "house", "4motif-diamond"])
+def test_exact_count_shards(agpm, oracle, pattern, nshards):
+    """Multi-GPU exact counting: every shard equals the oracle's
+    count of the same interleaved 32-arc chunks, and the shards sum to exact_count."""
+    g = agpm.rmat(11, 8, seed=9).relabel_by_degree()
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan(pattern)
+    dg = agpm.DeviceGraph(g)
+    parts = [agpm.exact_count_shard(dg, plan, r, nshards) for r in range(nshards)]
+    for r, c in enumerate(parts):
+        assert c == oracle.exact_count_shard(off, nbr, g.edge_count, plan, r, nshards)
+    assert sum(parts) == agpm.exact_count(dg, plan)
+    o = g.orient_by_degree()  # oriented clique DAG: every arc a seed
+    if plan.n_edges == plan.k * (plan.k - 1) // 2:
+        odg = agpm.DeviceGraph(o)
+        assert sum(agpm.exact_count_shard(odg, plan, r, nshards) for r in range(nshards)) == \
+            agpm.exact_count(odg, plan)
+    with pytest.raises(ValueError):
+        agpm.exact_count_shard(dg, plan, nshards, nshards)

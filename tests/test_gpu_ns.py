@@ -42,11 +42,11 @@ def strategy(agpm, request):
     agpm.set_frontier_reuse(request.param == "frontier_reuse")
     # frontier: the dense-core bit matrix covers every vertex of the small test
     # graphs by default; "nocore" runs the splitter-search path instead
-    agpm.set_core_dim(0 if request.param.endswith("nocore") else 32768)
+    agpm.set_core_dim(0 if request.param.endswith("nocore") else 65536)
     yield request.param
     agpm.set_strategy("auto")
     agpm.set_frontier_reuse(False)
-    agpm.set_core_dim(32768)
+    agpm.set_core_dim(65536)
 
 
 @pytest.mark.parametrize("name", ["er200", "er200_rel", "er60_dense", "rmat12_rel", "rmat12"])
@@ -81,12 +81,12 @@ def test_long_drivers_bit_exact(agpm, oracle, pattern, relabel, strat):
     plan = agpm.compile_plan(pattern)
     dg = agpm.DeviceGraph(g)
     agpm.set_strategy(strat.split("_")[0])
-    agpm.set_core_dim(0 if strat.endswith("nocore") else 32768)
+    agpm.set_core_dim(0 if strat.endswith("nocore") else 65536)
     try:
         v, h, b = agpm.draw_samples(dg, plan, 4, 777, 20000)
     finally:
         agpm.set_strategy("auto")
-        agpm.set_core_dim(32768)
+        agpm.set_core_dim(65536)
     ov, oh, ob = oracle.draw_records(off, nbr, g.edge_count, plan, 4, 777, 20000)
     np.testing.assert_array_equal(v, ov)
     np.testing.assert_array_equal(b, ob)

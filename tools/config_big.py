@@ -26,6 +26,9 @@ def main():
     ap.add_argument("--delta", type=float, default=0.05)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--repeats", type=int, default=3)
+    ap.add_argument("--strategy", default="auto")
+    ap.add_argument("--core", type=int, default=65536)
+    ap.add_argument("--skip-online", action="store_true")
     args = ap.parse_args()
     import torch
     torch.cuda.init()
@@ -36,17 +39,36 @@ def main():
     t_ingest = time.perf_counter() - t0
     info = dg.info()
     plan = agpm.compile_plan(args.pattern)
+    agpm.set_strategy(args.strategy)
+    agpm.set_core_dim(args.core)
     runs = []
-    for r in range(args.repeats):
+    for r in range(0 if args.skip_online else args.repeats):
         agpm.sync()
         t0 = time.perf_counter()
         res = agpm.run_ns_online(dg, plan, args.eps, args.delta, agpm.OnlinePolicy(), seed=args.seed + r)
         agpm.sync()
         runs.append({"seconds": time.perf_counter() - t0, "n": res.report.n, "estimate": res.report.mu,
                      "rel_err_bound": res.report.epsilon_hat, "converged": bool(res.report.converged)})
+    # fixed-budget throughput: 2^24-sample launches, CUDA events on the launching stream
+    B = 1 << 24
+    vals = torch.empty(B, dtype=torch.float64, device="cuda")
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
+    agpm.sample_dev(dg, plan, args.seed, 0, B, vals.data_ptr(), st.cuda_stream)  # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for r in range(3):
+        agpm.sample_dev(dg, plan, args.seed, (r + 1) * B, B, vals.data_ptr(), st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
     print(json.dumps({"workload": f"rmat{args.scale}_ef{args.edge_factor}_relabelled_{args.pattern}",
+                      "strategy": args.strategy, "core_dim": args.core,
                       "ingest_seconds": t_ingest, "graph": info,
-                      "free_gb_after_ingest": torch.cuda.mem_get_info()[0] / 1e9, "online": runs}))
+                      "free_gb_after_ingest": torch.cuda.mem_get_info()[0] / 1e9, "online": runs,
+                      "fixed_budget": {"samples": B, "ms": ms, "samples_per_s": B / (ms / 1e3),
+                                       "hit_rate": float((vals != 0).double().mean().item())}}))
 
 
 if __name__ == "__main__":
