@@ -379,13 +379,13 @@ __device__ __forceinline__ bool warp_contains(uint32_t b, uint32_t a) {
 }
 
 template <int K>
-__device__ __forceinline__ unsigned live_word(const FrontierArgs& A, const IsectDesc<K>& d, uint32_t core, uint32_t w,
-                                              int lane, int j) {
-  const uint32_t* __restrict__ nbr = A.g.nbr;
+__device__ __forceinline__ unsigned live_word_g(const GraphArgs& g, const IsectDesc<K>& d, uint32_t core, uint32_t w,
+                                                int lane, int j) {
+  const uint32_t* __restrict__ nbr = g.nbr;
   const uint32_t o = w * 32 + lane;
   const bool valid = o < d.dsize;
   const uint32_t a = valid ? ldo(d.drv, o) : INF;
-  if (core && !(core >> 31) && __shfl_sync(FULL, a, 0) < A.g.core_base) core = 0;
+  if (core && !(core >> 31) && __shfl_sync(FULL, a, 0) < g.core_base) core = 0;
   bool fail = !valid;
 #pragma unroll
   for (int q = 0; q < K - 1; ++q) {
@@ -393,7 +393,7 @@ __device__ __forceinline__ unsigned live_word(const FrontierArgs& A, const Isect
     if (!((d.lists >> q) & 1u)) continue;
     bool found;
     if ((core >> q) & 1u) {
-      found = valid && core_has_edge(A.g, d.owner[q], a);
+      found = valid && core_has_edge(g, d.owner[q], a);
     } else {
       const uint32_t* B = nbr + d.start[q];
       const uint32_t nb = d.len[q];
@@ -418,6 +418,12 @@ __device__ __forceinline__ unsigned live_word(const FrontierArgs& A, const Isect
     fail = fail || (found == (bool)((d.outs >> q) & 1u));
   }
   return __ballot_sync(FULL, !fail);
+}
+
+template <int K>
+__device__ __forceinline__ unsigned live_word(const FrontierArgs& A, const IsectDesc<K>& d, uint32_t core, uint32_t w,
+                                              int lane, int j) {
+  return live_word_g<K>(A.g, d, core, w, lane, j);
 }
 
 }  // namespace

@@ -62,6 +62,43 @@ __device__ __forceinline__ unsigned seg_mask(uint32_t w, uint32_t b0, uint32_t b
   return upto & ~((1u << lo) - 1u);
 }
 
+// A long driver, the whole warp on one sample: count the live elements, draw r
+// with the sample's stream (lane src), replay the words up to the r-th. Kept
+// out of line: it is rare, and inlined its registers would weigh on the hot loop.
+struct WpsOut {
+  unsigned long long cnt, ctr;
+  uint32_t o_pick;
+};
+
+template <int K>
+__device__ __noinline__ WpsOut wps_sample(const GraphArgs g, const IsectDesc<K>* dp, int lane, int src, int j,
+                                          unsigned long long key, unsigned long long ctr) {
+  const IsectDesc<K>& d = *dp;
+  const uint32_t core = d.core;
+  const uint32_t nw = (d.dsize + 31) >> 5;
+  unsigned long long c = 0;
+  for (uint32_t w = 0; w < nw; ++w) c += __popc(live_word_g<K>(g, d, core, w, lane, j));
+  CounterRng rr(0);
+  rr.key = key;
+  rr.ctr = ctr;
+  unsigned long long r = 0;
+  if (lane == src && c) r = rr.next_below(c);
+  r = __shfl_sync(FULL, r, src);
+  uint32_t op = 0;
+  if (c) {
+    for (uint32_t w = 0; w < nw; ++w) {
+      const unsigned live = live_word_g<K>(g, d, core, w, lane, j);
+      const unsigned pc = __popc(live);
+      if (r < pc) {
+        op = w * 32 + __fns(live, 0, (int)r + 1);
+        break;
+      }
+      r -= pc;
+    }
+  }
+  return WpsOut{c, rr.ctr, op};
+}
+
 template <int K, int kFlatU, int kMinB>
 __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const FrontierArgs A) {
   __shared__ IsectDesc<K> sdesc[kFlatThreads];
@@ -119,29 +156,11 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       // the r-th live element
       for (unsigned bm = __ballot_sync(FULL, wps); bm; bm &= bm - 1) {
         const int src = __ffs(bm) - 1;
-        const IsectDesc<K>& d = wdesc[src];
-        const uint32_t core = d.core;
-        const uint32_t nw = (d.dsize + 31) >> 5;
-        unsigned long long c = 0;
-        for (uint32_t w = 0; w < nw; ++w) c += __popc(live_word<K>(A, d, core, w, lane, j));
-        unsigned long long r = 0;
-        if (lane == src && c) r = S.rng.next_below(c);
-        r = __shfl_sync(FULL, r, src);
-        uint32_t op = 0;
-        if (c) {
-          for (uint32_t w = 0; w < nw; ++w) {
-            const unsigned live = live_word<K>(A, d, core, w, lane, j);
-            const unsigned pc = __popc(live);
-            if (r < pc) {
-              op = w * 32 + __fns(live, 0, (int)r + 1);
-              break;
-            }
-            r -= pc;
-          }
-        }
+        const WpsOut o = wps_sample<K>(A.g, wdesc + src, lane, src, j, S.rng.key, S.rng.ctr);
         if (lane == src) {
-          cnt = c;
-          o_pick = op;
+          cnt = o.cnt;
+          o_pick = o.o_pick;
+          S.rng.ctr = o.ctr;
         }
       }
       // fast path (the common case on a relabelled graph): every other list is a
