@@ -63,12 +63,22 @@ def main():
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
+    # SURVEY §8(d) B_min sector model on this graph (device replay of 2^22 sample paths)
+    bmin = agpm.bmin_bytes(dg, plan, args.seed, 0, 1 << 22, st.cuda_stream) / float(1 << 22)
+    peak = 6531.9
+    try:
+        with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) as f:
+            peak = json.load(f)["hbm_gbs"]
+    except Exception:
+        pass
     print(json.dumps({"workload": f"rmat{args.scale}_ef{args.edge_factor}_relabelled_{args.pattern}",
                       "strategy": args.strategy, "core_dim": args.core,
                       "ingest_seconds": t_ingest, "graph": info,
                       "free_gb_after_ingest": torch.cuda.mem_get_info()[0] / 1e9, "online": runs,
                       "fixed_budget": {"samples": B, "ms": ms, "samples_per_s": B / (ms / 1e3),
-                                       "hit_rate": float((vals != 0).double().mean().item())}}))
+                                       "hit_rate": float((vals != 0).double().mean().item()),
+                                       "bmin_bytes_per_sample": bmin,
+                                       "roofline_frac": bmin * B / (ms / 1e3) / 1e9 / peak}}))
 
 
 if __name__ == "__main__":
