@@ -2,6 +2,10 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <unordered_map>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -19,18 +23,65 @@ DeviceCtx* g_ctx[64] = {nullptr};
 
 void set_last_error(const std::string& msg) { t_err = msg; }
 
+// Large blocks (32 MB .. 1 GB) freed by dev_free are parked here, up to 4 GB per
+// process, and handed back to the next dev_malloc of the same size: recreating a
+// graph view (the e2e loop) then reuses its buffers outright. The stream-ordered
+// pool alone periodically took 20-55 ms to hand back the 512 MB core matrix.
+namespace {
+struct Parked {
+  void* p;
+  size_t bytes;
+  int device;
+};
+std::mutex g_park_mu;
+std::vector<Parked> g_parked;
+std::unordered_map<void*, size_t> g_big;  // live large blocks -> size
+size_t g_parked_bytes = 0;
+constexpr size_t kParkMin = 32ull << 20, kParkMax = 1ull << 30, kParkCap = 4ull << 30;
+}  // namespace
+
 cudaError_t dev_malloc_bytes(void** p, size_t bytes) {
-  cudaStream_t s = ctx_for_current_device().stream;
-  cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, s);
+  DeviceCtx& ctx = ctx_for_current_device();
+  if (bytes >= kParkMin && bytes <= kParkMax) {
+    std::lock_guard<std::mutex> lk(g_park_mu);
+    for (size_t i = 0; i < g_parked.size(); ++i)
+      if (g_parked[i].bytes == bytes && g_parked[i].device == ctx.device) {
+        *p = g_parked[i].p;
+        g_parked_bytes -= bytes;
+        g_parked.erase(g_parked.begin() + (long)i);
+        g_big[*p] = bytes;
+        return cudaSuccess;
+      }
+  }
+  cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, ctx.stream);
   if (e != cudaSuccess) return e;
-  return cudaStreamSynchronize(s);
+  e = cudaStreamSynchronize(ctx.stream);
+  if (e == cudaSuccess && bytes >= kParkMin && bytes <= kParkMax) {
+    std::lock_guard<std::mutex> lk(g_park_mu);
+    g_big[*p] = bytes;
+  }
+  return e;
 }
 
 cudaError_t dev_free(void* p) {
   if (!p) return cudaSuccess;
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return e;
-  return cudaFreeAsync(p, ctx_for_current_device().stream);
+  DeviceCtx& ctx = ctx_for_current_device();
+  {
+    std::lock_guard<std::mutex> lk(g_park_mu);
+    auto it = g_big.find(p);
+    if (it != g_big.end()) {
+      const size_t bytes = it->second;
+      g_big.erase(it);
+      if (g_parked_bytes + bytes <= kParkCap) {  // idle (device synchronised above): reusable at once
+        g_parked.push_back({p, bytes, ctx.device});
+        g_parked_bytes += bytes;
+        return cudaSuccess;
+      }
+    }
+  }
+  return cudaFreeAsync(p, ctx.stream);
 }
 void count_launch(uint64_t n) { g_launches += n; }
 
