@@ -318,11 +318,12 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
     A.step_multi[st] = !(__builtin_popcount(in_m) == 1 && out_m == 0);
     A.step_reuse[st] = 0;
   }
-  // 2 words in flight per warp; registers capped for 10 (k <= 4) or 8 resident
-  // 128-thread blocks per SM: the loop is latency bound, so occupancy beats the
-  // few spills the cap costs (measured on config 2: 96 regs 14.2 ms, 64 regs
-  // 9.7 ms, 48 regs 9.4 ms, 40 regs 9.9 ms per 2^24 samples)
-  constexpr int kMinB = K <= 4 ? 10 : 8;
+  // 2 words in flight per warp; registers capped by the resident 128-thread
+  // blocks per SM: the loop is latency bound, so occupancy beats the few spills
+  // a cap costs. Measured per 2^24 samples on the config-2 graph: 4-clique 96
+  // regs 14.2 ms, 64 regs 9.1, 56 regs 8.9, 48 regs 8.8, 40 regs 9.9; triangle
+  // 64 regs 5.5 vs 48 regs 5.8; 5-clique 48 regs 12.3 vs 64 regs 13.4.
+  constexpr int kMinB = K == 3 ? 8 : K <= 5 ? 10 : 8;
   auto kern = fr_flat_kernel<K, 2, kMinB>;
   static int occ = -1;
   if (occ < 0) {
