@@ -176,3 +176,24 @@ def test_values_without_bindings(agpm, oracle, graphs, pattern, strategy):
     v, h, _ = agpm.draw_samples(agpm.DeviceGraph(g), plan, 4, 999, 5000, with_bindings=False)
     ov, oh, _ = oracle.draw_records(off, nbr, g.edge_count, plan, 4, 999, 5000)
     np.testing.assert_array_equal(v, ov)
+
+
+@pytest.mark.parametrize("pattern", ["7clique", "8clique", "9clique"])
+@pytest.mark.parametrize("strat", ["flat", "frontier", "warp"])
+def test_large_k_bit_exact(agpm, oracle, pattern, strat):
+    """k = 7..9 instantiations (the register-capped flat kernels spill most
+    there) on a dense graph where deep cliques are common: values, hits and
+    bindings match the oracle record for record."""
+    g = agpm.er_graph(48, 0.7, 13).relabel_by_degree()
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan(pattern)
+    dg = agpm.DeviceGraph(g)
+    agpm.set_strategy(strat)
+    try:
+        v, h, b = agpm.draw_samples(dg, plan, 3, 99, 3000)
+    finally:
+        agpm.set_strategy("auto")
+    ov, oh, ob = oracle.draw_records(off, nbr, g.edge_count, plan, 3, 99, 3000)
+    assert np.count_nonzero(oh) > 0
+    np.testing.assert_array_equal(v, ov)
+    np.testing.assert_array_equal(b, ob)
