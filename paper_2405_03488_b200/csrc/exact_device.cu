@@ -72,6 +72,7 @@ __device__ __forceinline__ bool warp_member(const uint32_t* B, uint32_t nb, uint
   return at < nb && ldn(B, at) == a;
 }
 
+
 template <int K>
 __global__ void __launch_bounds__(256) exact_kernel(const GraphArgs g, const DevPlan p, const int apply_bounds,
                                                     const int skip_unordered, const uint32_t root_limit,
@@ -157,11 +158,44 @@ __global__ void __launch_bounds__(256) exact_kernel(const GraphArgs g, const Dev
             }
           }
         }
+        const bool last = ss == L - 1;
+        if (last && g.core && out_m == 0 && lo >= g.core_base && dsize > 0) {
+          // leaf whose lists are all dense-core rows over a range inside the core:
+          // |S| = popcount of the AND of the rows over [lo, hi) minus the bound
+          // vertices in it — coalesced row words instead of one search per element.
+          // Taken when the row words are at most 4x the driver elements (factors
+          // 1..16 measured within 5 % of each other on RMAT-18/20).
+          bool rows_ok = true;
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if (q < j && ((in_m >> q) & 1u) && bnd[q] < g.core_base) rows_ok = false;
+          const uint32_t lo_c = lo - g.core_base;
+          const uint32_t hi_c = min(hi, g.core_base + g.core_wpr * 32u) - g.core_base;
+          const uint32_t w0 = lo_c >> 5, w1 = hi_c > lo_c ? (hi_c + 31) >> 5 : w0;
+          if (rows_ok && (w1 - w0) <= 4 * dsize) {
+            uint32_t cnt = 0;
+            for (uint32_t w = w0 + lane; w < w1; w += 32) {
+              unsigned x = FULL;
+#pragma unroll
+              for (int q = 0; q < K; ++q)
+                if (q < j && ((in_m >> q) & 1u))
+                  x &= __ldg(g.core + (unsigned long long)(bnd[q] - g.core_base) * g.core_wpr + w);
+              if (w == w0) x &= ~((1u << (lo_c & 31)) - 1u);
+              if (w == w1 - 1 && (hi_c & 31)) x &= (1u << (hi_c & 31)) - 1u;
+#pragma unroll
+              for (int q = 0; q < K; ++q)
+                if (q < j && bnd[q] >= lo && bnd[q] < hi && ((bnd[q] - g.core_base) >> 5) == w)
+                  x &= ~(1u << ((bnd[q] - g.core_base) & 31));  // bound vertices are not candidates
+              cnt += __popc(x);
+            }
+            res = __reduce_add_sync(FULL, cnt);
+            continue;
+          }
+        }
         const uint32_t* D = nbr;
 #pragma unroll
         for (int q = 0; q < K; ++q)
           if (q == drv) D = nbr + pb[q] + rs[q];
-        const bool last = ss == L - 1;
         uint32_t* out = buf + (unsigned long long)(last ? 0 : ss) * cap;
         uint32_t n = 0;
         for (uint32_t c0 = 0; c0 < dsize; c0 += 32) {
@@ -248,7 +282,12 @@ template <int K>
 unsigned long long run_exact_k(const agpm_graph* gr, const DevPlan& p, bool apply_bounds, bool skip_unordered,
                                uint32_t root_limit, uint32_t shard, uint32_t nshards, cudaStream_t s) {
   DeviceCtx& ctx = ctx_for_current_device();
+  // the dense-core bit matrix (core_bits.cu) answers leaves whose lists are core rows
+  ensure_core_bits(const_cast<agpm_graph*>(gr), s);
   GraphArgs g{gr->vtx, gr->nbr, gr->seed_arcs, gr->arcs, gr->plain, nullptr, 0};
+  g.core = gr->core;
+  g.core_base = gr->core_base;
+  g.core_wpr = gr->core_wpr;
   int occ = 0;
   AGPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, exact_kernel<K>, 256, 0));
   occ = std::max(occ, 1);
