@@ -79,27 +79,55 @@ __device__ agpm_report predicted_error_dev(const agpm_accumulator& a, double z) 
   return r;
 }
 
-// Sequential merge of window partials in window order (ns_engine.cpp:121-137)
-__global__ void converge_kernel(const agpm_accumulator* __restrict__ win, unsigned long long nwin,
-                                OnlineState* st, double z, double eps, unsigned long long max_samples) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Merge of window partials in window order (ns_engine.cpp:121-137). The running
+// accumulator is the reference's left fold (one thread adds the windows of a
+// 256-window chunk in order, exactly as before); the per-window stop tests —
+// a division, a square root and two more divisions each, the slow part —
+// run one window per thread, and the first window that stops wins. Same sums,
+// same reports, same stop window as the one-thread loop.
+constexpr int kConvergeThreads = 256;
+__global__ void __launch_bounds__(kConvergeThreads) converge_kernel(const agpm_accumulator* __restrict__ win,
+                                                                    unsigned long long nwin, OnlineState* st,
+                                                                    double z, double eps,
+                                                                    unsigned long long max_samples) {
+  __shared__ agpm_accumulator pre[kConvergeThreads];
+  __shared__ agpm_accumulator chunk[kConvergeThreads];
+  __shared__ int first;
+  const int t = threadIdx.x;
   OnlineState s = *st;
-  for (unsigned long long w = 0; w < nwin && !s.stopped; ++w) {
-    const agpm_accumulator a = win[w];
-    s.acc.n += a.n;
-    s.acc.hits += a.hits;
-    s.acc.sum = __dadd_rn(s.acc.sum, a.sum);
-    s.acc.squared_sum = __dadd_rn(s.acc.squared_sum, a.squared_sum);
-    ++s.windows;
+  for (unsigned long long w0 = 0; w0 < nwin && !s.stopped; w0 += kConvergeThreads) {
+    const int cnt = (int)min((unsigned long long)kConvergeThreads, nwin - w0);
+    if (t < cnt) chunk[t] = win[w0 + t];
+    if (t == 0) first = kConvergeThreads;
+    __syncthreads();
+    if (t == 0) {  // the left fold, in window order
+      agpm_accumulator acc = s.acc;
+      for (int i = 0; i < cnt; ++i) {
+        acc.n += chunk[i].n;
+        acc.hits += chunk[i].hits;
+        acc.sum = __dadd_rn(acc.sum, chunk[i].sum);
+        acc.squared_sum = __dadd_rn(acc.squared_sum, chunk[i].squared_sum);
+        pre[i] = acc;
+      }
+    }
+    __syncthreads();
+    if (t < cnt) {
+      const agpm_report r = predicted_error_dev(pre[t], z);
+      if (r.epsilon_hat <= eps || pre[t].n >= max_samples) atomicMin(&first, t);
+    }
+    __syncthreads();
+    const int stop = first;
+    const int last = stop < cnt ? stop : cnt - 1;
+    s.acc = pre[last];
+    s.windows += (unsigned long long)last + 1;
     s.rep = predicted_error_dev(s.acc, z);
-    if (s.rep.epsilon_hat <= eps) {
-      s.rep.converged = 1;
-      s.stopped = 1;
-    } else if (s.acc.n >= max_samples) {
+    if (stop < cnt) {
+      if (s.rep.epsilon_hat <= eps) s.rep.converged = 1;
       s.stopped = 1;
     }
+    __syncthreads();  // chunk / pre / first are rewritten by the next chunk
   }
-  *st = s;
+  if (t == 0) *st = s;
 }
 
 // ------------------------------------------------------------ host side
@@ -405,7 +433,7 @@ int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delt
       const uint64_t nw = (c + window - 1) / window;
       enqueue_sample(g, dp, seed, launched, c, d_values, nullptr, nullptr, s);
       enqueue_moments(d_values, c, window, d_win, s);
-      converge_kernel<<<1, 32, 0, s>>>(d_win, nw, d_state, z, eps, pol.max_samples);
+      converge_kernel<<<1, kConvergeThreads, 0, s>>>(d_win, nw, d_state, z, eps, pol.max_samples);
       count_launch();
       AGPM_CUDA(cudaGetLastError());
       AGPM_CUDA(cudaMemcpyAsync(h_state, d_state, sizeof(OnlineState), cudaMemcpyDeviceToHost, s));
