@@ -25,29 +25,37 @@ namespace {
 
 uint32_t g_core_dim = 65536;
 
-// one warp per core row: build the row in shared memory, then write it out
+// one block per core row: the row is built in shared memory (zeroed, one
+// shared atomic per core neighbour) and written out with 16-B stores
 __global__ void __launch_bounds__(256) core_rows_kernel(const VtxInfo* __restrict__ vtx,
                                                         const uint32_t* __restrict__ nbr, uint32_t base,
                                                         uint32_t rows, uint32_t wpr, uint32_t* __restrict__ bits) {
-  extern __shared__ uint32_t sh[];
+  extern __shared__ uint32_t row[];
+  __shared__ uint32_t s_start;
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  uint32_t* row = sh + (size_t)wib * wpr;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
-    for (uint32_t i = lane; i < wpr; i += 32) row[i] = 0;
-    __syncwarp();
+  for (uint32_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (uint32_t i = threadIdx.x; i < wpr; i += blockDim.x) row[i] = 0;
     const VtxInfo vi = load_vtx(vtx, base + r);
     const uint32_t* list = nbr + vi.begin;
-    const uint32_t start = kary_lb(list, 0, vi.deg, base, lane, nullptr);
-    for (uint32_t i = start + lane; i < vi.deg; i += 32) {
+    if (threadIdx.x < 32) {
+      const uint32_t start = kary_lb(list, 0, vi.deg, base, lane, nullptr);
+      if (lane == 0) s_start = start;
+    }
+    __syncthreads();
+    for (uint32_t i = s_start + threadIdx.x; i < vi.deg; i += blockDim.x) {
       const uint32_t c = __ldg(list + i) - base;
       atomicOr(row + (c >> 5), 1u << (c & 31));
     }
-    __syncwarp();
+    __syncthreads();
     uint32_t* out = bits + (unsigned long long)r * wpr;
-    for (uint32_t i = lane; i < wpr; i += 32) out[i] = row[i];
-    __syncwarp();
+    if ((wpr & 3) == 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(row);
+      uint4* dst = reinterpret_cast<uint4*>(out);
+      for (uint32_t i = threadIdx.x; i < wpr / 4; i += blockDim.x) dst[i] = src[i];
+    } else {
+      for (uint32_t i = threadIdx.x; i < wpr; i += blockDim.x) out[i] = row[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -72,10 +80,10 @@ void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
   const uint32_t wpr = (want + 31) / 32;
   uint32_t* bits = nullptr;
   AGPM_CUDA(dev_malloc(&bits, 4ull * wpr * want));
-  const size_t shmem = 8ull * 4 * wpr;
+  const size_t shmem = 4ull * wpr;
   if (shmem > 48 * 1024)
     AGPM_CUDA(cudaFuncSetAttribute(core_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
-  const unsigned blocks = std::max(1u, std::min((want + 7) / 8, (unsigned)ctx.sm_count * 4));
+  const unsigned blocks = std::max(1u, std::min(want, (unsigned)ctx.sm_count * 8));
   core_rows_kernel<<<blocks, 256, shmem, s>>>(g->vtx, g->nbr, base, want, wpr, bits);
   count_launch();
   AGPM_CUDA(cudaGetLastError());
