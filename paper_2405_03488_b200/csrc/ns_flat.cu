@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
   __shared__ uint32_t sbal[kFlatThreads / 32][kFlatW];
   __shared__ uint32_t smap[kFlatThreads / 32][32];
   __shared__ uint4 sfast[kFlatThreads];
+  __shared__ uint32_t sexcl[kFlatThreads];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   IsectDesc<K>* wdesc = sdesc + (threadIdx.x & ~31u);
   IsectDesc<K>& my = wdesc[lane];
@@ -171,12 +172,6 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       if (pend >= 0 && !wps) {
         const uint32_t l = my.lists;
         fast = my.core == (l | (1u << 31)) && my.outs == 0 && my.exb == 0 && __popc(l) <= 2;
-        if (fast) {
-          const int q0 = __ffs(l) - 1, q1 = 31 - __clz(l);
-          const unsigned long long dp = reinterpret_cast<unsigned long long>(my.drv);
-          sfast[threadIdx.x] = make_uint4((uint32_t)dp, (uint32_t)(dp >> 32), (my.owner[q0] - cb) * A.g.core_wpr,
-                                          (my.owner[q1] - cb) * A.g.core_wpr);
-        }
       }
       // the rest: flattened element-parallel rounds of <= kFlatW * 32 elements,
       // fast samples first, then the others (each class flattened on its own)
@@ -195,10 +190,23 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       if (total == 0) continue;
       const unsigned partm = __ballot_sync(FULL, part);
       __syncwarp();
-      if (part) smap[wid][__popc(partm & lt_mask)] = (uint32_t)lane;
+      if (part) {
+        const uint32_t rank = __popc(partm & lt_mask);
+        smap[wid][rank] = (uint32_t)lane;
+        if (allfast) {  // the fast table is indexed by segment rank: no lane lookup in the loop
+          const uint32_t l = my.lists;
+          const int q0 = __ffs(l) - 1, q1 = 31 - __clz(l);
+          const unsigned long long dp = reinterpret_cast<unsigned long long>(my.drv);
+          sfast[(threadIdx.x & ~31u) + rank] = make_uint4((uint32_t)dp, (uint32_t)(dp >> 32),
+                                                          (my.owner[q0] - cb) * A.g.core_wpr,
+                                                          (my.owner[q1] - cb) * A.g.core_wpr);
+          sexcl[(threadIdx.x & ~31u) + rank] = excl;
+        }
+      }
       __syncwarp();
       const uint32_t lane_of_rank = smap[wid][lane];
       const uint4* wfast = sfast + (threadIdx.x & ~31u);
+      const uint32_t* wexcl = sexcl + (threadIdx.x & ~31u);
       for (uint32_t R0 = 0; R0 < total;) {
         const uint32_t Rend = __reduce_max_sync(FULL, P <= R0 + (uint32_t)kFlatW * 32 ? P : 0u);
         uint32_t rk = __popc(__ballot_sync(FULL, part && P <= R0));  // segments of earlier rounds
@@ -215,9 +223,8 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
                   __reduce_or_sync(FULL, (part && excl >= eb && excl < eb + 32) ? 1u << (excl - eb) : 0u);
               const uint32_t rank = rk + __popc(starts & ((2u << lane) - 1u)) - 1u;
               rk += __popc(starts);
-              const int src = (int)__shfl_sync(FULL, lane_of_rank, (int)(rank & 31u));
-              const uint32_t ex_src = __shfl_sync(FULL, excl, src);
-              const uint4 f = wfast[src];
+              const uint4 f = wfast[rank & 31u];
+              const uint32_t ex_src = wexcl[rank & 31u];
               v[u] = eb + lane < Rend;
               const uint32_t* drv = reinterpret_cast<const uint32_t*>(((unsigned long long)f.y << 32) | f.x);
               a[u] = v[u] ? ldo(drv, eb + lane - ex_src) - cb : 0u;
