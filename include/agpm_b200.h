@@ -223,6 +223,12 @@ int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delt
  * intersects the concatenation of the pending samples' drivers element-parallel,
  * picks lane-parallel). All strategies draw identical samples. */
 int agpm_ns_set_strategy(int strategy);
+/* Per-sample stream policy: 0 = CounterRng(seed, 0, sample_id) (default; the
+ * reference's stream, bit-exact with its draw_sample), 1 = Philox4x32-10 keyed by
+ * the seed with counter (draw index, sample id) — a counter-based stream of the
+ * same (seed, id) addressing; eager plans on the flat sampler only (other
+ * strategies raise AGPM_E_INVALID). */
+int agpm_ns_set_rng(int policy);
 /* frontier only: let a step whose lists nest the previous step's (cliques)
  * intersect that step's survivors instead of recomputing (same samples). */
 int agpm_ns_set_frontier_reuse(int on);

@@ -39,14 +39,51 @@ uint64_t orc_derive_key(uint64_t seed, uint64_t s1, uint64_t s2) { /* rng.hpp:19
 }
 
 typedef struct {
-  uint64_t key, ctr;
+  uint64_t key, ctr, id;
+  int philox; /* 0: the reference's CounterRng; 1: the builder's optional Philox policy */
 } orc_rng;
 
 static orc_rng rng_make(uint64_t seed, uint64_t s1, uint64_t s2) { /* rng.hpp:28-29 */
-  orc_rng r = {orc_derive_key(seed, s1, s2), 0};
+  orc_rng r = {orc_derive_key(seed, s1, s2), 0, 0, 0};
   return r;
 }
+
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11): ten rounds of
+ * (hi, lo) = M * c for c0, c2 with M = 0xD2511F53 / 0xCD9E8D57, the outputs
+ * recombined with c1, c3 and the key, the key bumped by the Weyl constants
+ * 0x9E3779B9 / 0xBB67AE85 between rounds. Restated for the device's optional
+ * Philox stream (csrc/rng.cuh); not part of the reference. */
+void orc_philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+    uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+    c[1] = (uint32_t)p1;
+    c[3] = (uint32_t)p0;
+    c[0] = n0;
+    c[2] = n2;
+  }
+}
+
+/* the device's Philox stream: draw t of sample id under seed s is block
+ * (counter (t, id), key s), low 64 bits */
+static orc_rng rng_make_philox(uint64_t seed, uint64_t id) {
+  orc_rng r = {seed, 0, id, 1};
+  return r;
+}
+
 static uint64_t rng_u64(orc_rng* r) { /* rng.hpp:31-34 */
+  if (r->philox) {
+    uint32_t c[4] = {(uint32_t)r->ctr, (uint32_t)(r->ctr >> 32), (uint32_t)r->id, (uint32_t)(r->id >> 32)};
+    ++r->ctr;
+    orc_philox4x32_10(c, (uint32_t)r->key, (uint32_t)(r->key >> 32));
+    return (uint64_t)c[0] | ((uint64_t)c[1] << 32);
+  }
   r->ctr += 0x9e3779b97f4a7c15ull;
   return mix64(r->key ^ r->ctr);
 }
@@ -444,17 +481,36 @@ static int draw_one(const view_t* g, const seed_index_t* si, const agpm_plan* pl
 
 /* Per-sample records for stream (seed, worker, first+i): value, hit, bindings
  * (k per sample, 0xffffffff past a miss). Mirrors draw_sample (ns_engine.cpp:92-104). */
+static int draw_records_impl(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t* end,
+                             const uint32_t* nbr, const agpm_plan* plan, uint64_t seed, uint64_t worker,
+                             uint64_t first, uint64_t count, double* values, uint8_t* hits,
+                             uint32_t* bindings, int philox);
+
 int orc_draw_records(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t* end,
                      const uint32_t* nbr, const agpm_plan* plan, uint64_t seed, uint64_t worker,
                      uint64_t first, uint64_t count, double* values, uint8_t* hits,
                      uint32_t* bindings) {
+  return draw_records_impl(n, m, begin, end, nbr, plan, seed, worker, first, count, values, hits, bindings, 0);
+}
+
+/* the same records under the optional Philox stream (keyed by seed, counter (draw, id)) */
+int orc_draw_records_philox(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t* end,
+                            const uint32_t* nbr, const agpm_plan* plan, uint64_t seed, uint64_t first,
+                            uint64_t count, double* values, uint8_t* hits, uint32_t* bindings) {
+  return draw_records_impl(n, m, begin, end, nbr, plan, seed, 0, first, count, values, hits, bindings, 1);
+}
+
+static int draw_records_impl(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t* end,
+                             const uint32_t* nbr, const agpm_plan* plan, uint64_t seed, uint64_t worker,
+                             uint64_t first, uint64_t count, double* values, uint8_t* hits,
+                             uint32_t* bindings, int philox) {
   view_t g = mkview(n, m, begin, end, nbr, 0);
   if (g.m == 0) return AGPM_E_INVALID;
   seed_index_t si = seed_index(&g);
   scratch_t s = {{0, 0, 0}, {0, 0, 0}};
   uint32_t b[AGPM_MAX_K];
   for (uint64_t i = 0; i < count; ++i) {
-    orc_rng rng = rng_make(seed, worker, first + i);
+    orc_rng rng = philox ? rng_make_philox(seed, first + i) : rng_make(seed, worker, first + i);
     double val;
     int nb = draw_one(&g, &si, plan, &rng, b, &val, &s);
     values[i] = val;

@@ -28,7 +28,7 @@ __all__ = [
     "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
     "hit_rate_report", "exact_count", "exact_count_rooted", "region_split", "gs_estimate", "choose_keep_probability", "ns_cost_cone",
     "gs_cost_estimate", "select_scheme", "count_matches_through_edge", "estimate_gamma", "fast_profile",
-    "calibrate_hardware_constant", "count_hybrid", "exact_count_shard", "bmin_bytes", "set_strategy", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "calibrate_hardware_constant", "count_hybrid", "exact_count_shard", "bmin_bytes", "set_strategy", "set_rng", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
 ]
 
@@ -154,6 +154,7 @@ def _declare(L):
                                         C.POINTER(A.HybridResult), A.P]),
         "agpm_ns_set_frontier_reuse": (C.c_int, [C.c_int]),
         "agpm_ns_set_core_dim": (C.c_int, [A.u32]),
+        "agpm_ns_set_rng": (C.c_int, [C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -603,6 +604,12 @@ def set_strategy(name):
 def set_core_dim(dim):
     """Dense-core bit-matrix dimension for the frontier sampler (0 = off, default 65536)."""
     _check(lib().agpm_ns_set_core_dim(int(dim)))
+
+
+def set_rng(policy):
+    """Per-sample stream: "counter" (CounterRng, the reference's stream; default) or "philox"
+    (Philox4x32-10 keyed by the seed, counter (draw, sample id); flat sampler, eager plans)."""
+    _check(lib().agpm_ns_set_rng({"counter": 0, "philox": 1}.get(policy, -1)))
 
 
 def set_frontier_reuse(on):

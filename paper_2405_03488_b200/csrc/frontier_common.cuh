@@ -66,13 +66,13 @@ __device__ __forceinline__ uint32_t lb_thread(const uint32_t* base, uint32_t lo,
   return lo;
 }
 
-template <int K>
+template <int K, class R = CounterRng>
 struct Sample {
   uint32_t bnd[K], hbo[K], hbl[K];
   unsigned long long pb[K];
   uint32_t pd[K], up[K];
   bool loaded[K];
-  CounterRng rng;
+  R rng;
   double alpha;
   __device__ Sample(unsigned long long seed, unsigned long long id) : rng(seed, 0, id) {
 #pragma unroll
@@ -87,8 +87,8 @@ struct Sample {
   }
 };
 
-template <int K>
-__device__ __forceinline__ void ensure_vtx(const GraphArgs& g, Sample<K>& S, int q) {
+template <int K, class R>
+__device__ __forceinline__ void ensure_vtx(const GraphArgs& g, Sample<K, R>& S, int q) {
 #pragma unroll
   for (int t = 0; t < K; ++t)
     if (t == q && !S.loaded[t]) {
@@ -100,8 +100,8 @@ __device__ __forceinline__ void ensure_vtx(const GraphArgs& g, Sample<K>& S, int
     }
 }
 
-template <int K>
-__device__ __forceinline__ uint32_t lbq(const uint32_t* nbr, Sample<K>& S, int q, uint32_t x, bool update) {
+template <int K, class R>
+__device__ __forceinline__ uint32_t lbq(const uint32_t* nbr, Sample<K, R>& S, int q, uint32_t x, bool update) {
   uint32_t r = 0;
 #pragma unroll
   for (int t = 0; t < K; ++t)
@@ -118,8 +118,8 @@ __device__ __forceinline__ uint32_t lbq(const uint32_t* nbr, Sample<K>& S, int q
   return r;
 }
 
-template <int K>
-__device__ __forceinline__ void bind(Sample<K>& S, int q, uint32_t v) {
+template <int K, class R>
+__device__ __forceinline__ void bind(Sample<K, R>& S, int q, uint32_t v) {
 #pragma unroll
   for (int t = 0; t < K; ++t)
     if (t == q) {
@@ -130,8 +130,8 @@ __device__ __forceinline__ void bind(Sample<K>& S, int q, uint32_t v) {
     }
 }
 
-template <int K>
-__device__ void store_state(const FrontierArgs& A, unsigned long long i, const Sample<K>& S, int nb) {
+template <int K, class R>
+__device__ void store_state(const FrontierArgs& A, unsigned long long i, const Sample<K, R>& S, int nb) {
 #pragma unroll
   for (int q = 0; q < K; ++q)
     if (q < nb) {
@@ -143,8 +143,8 @@ __device__ void store_state(const FrontierArgs& A, unsigned long long i, const S
   A.alpha[i] = S.alpha;
 }
 
-template <int K>
-__device__ void load_state(const FrontierArgs& A, unsigned long long i, Sample<K>& S, int nb) {
+template <int K, class R>
+__device__ void load_state(const FrontierArgs& A, unsigned long long i, Sample<K, R>& S, int nb) {
 #pragma unroll
   for (int q = 0; q < K; ++q)
     if (q < nb) {
@@ -156,8 +156,8 @@ __device__ void load_state(const FrontierArgs& A, unsigned long long i, Sample<K
   S.alpha = A.alpha[i];
 }
 
-template <int K>
-__device__ void finish(const FrontierArgs& A, unsigned long long i, const Sample<K>& S, int nb, bool hit) {
+template <int K, class R>
+__device__ void finish(const FrontierArgs& A, unsigned long long i, const Sample<K, R>& S, int nb, bool hit) {
   A.values[i] = hit ? S.alpha : 0.0;
   if (A.work) A.work[i] = 0;
   if (A.bindings) {
@@ -167,8 +167,8 @@ __device__ void finish(const FrontierArgs& A, unsigned long long i, const Sample
 }
 
 // order bounds of step s from the current bindings (walker.hpp:64-69)
-template <int K>
-__device__ __forceinline__ void step_bounds(const DevPlan& p, int s, const Sample<K>& S, uint32_t& lo, uint32_t& hi) {
+template <int K, class R>
+__device__ __forceinline__ void step_bounds(const DevPlan& p, int s, const Sample<K, R>& S, uint32_t& lo, uint32_t& hi) {
   lo = 0;
   hi = INF;
 #pragma unroll
@@ -185,8 +185,8 @@ __device__ __forceinline__ void step_bounds(const DevPlan& p, int s, const Sampl
 // Returns the step whose descriptor was written (pending intersection), or -1
 // once the sample is finished. With `local` set (fused kernel) the descriptor
 // goes there and nothing is written to the SoA state.
-template <int K>
-__device__ int advance(const FrontierArgs& A, unsigned long long i, Sample<K>& S, int s0, const uint32_t* surv,
+template <int K, class R>
+__device__ int advance(const FrontierArgs& A, unsigned long long i, Sample<K, R>& S, int s0, const uint32_t* surv,
                        uint32_t surv_len, IsectDesc<K>* local = nullptr) {
   const uint32_t* __restrict__ nbr = A.g.nbr;
   const DevPlan& p = A.p;

@@ -241,6 +241,10 @@ int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count) {
   return count >= (1ull << 18) ? kStrategyFrontier : kStrategyWarp;
 }
 
+// per-sample stream: 0 = CounterRng(seed, 0, id) (the reference's stream, the
+// parity policy), 1 = Philox4x32-10 keyed by seed, counter (draw, id) — flat sampler
+int g_rng_policy = 0;
+
 // enqueue one sampling launch for ids [first, first+count) into d_values
 void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint64_t first, uint64_t count,
                     double* d_values, uint32_t* d_bindings, unsigned long long* d_bytes, cudaStream_t s) {
@@ -248,6 +252,15 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
   auto* cursor = static_cast<unsigned long long*>(ctx.get(0, 64));
   AGPM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
   if (dp.k < 3 || dp.k > AGPM_MAX_K) throw std::invalid_argument("device sampler needs 3 <= k <= 9");
+  if (g_rng_policy == 1) {  // Philox stream: the flat sampler, eager plans
+    if (dp.lazy || d_bytes) throw std::invalid_argument("the Philox stream runs on the eager flat sampler");
+    if (g_strategy != kStrategyAuto && g_strategy != kStrategyFlat)
+      throw std::invalid_argument("the Philox stream runs on the flat sampler (strategy auto or flat)");
+    ensure_core_bits(const_cast<agpm_graph*>(g), s);
+    SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, nullptr};
+    launch_ns_flat(L, s, true);
+    return;
+  }
   if (dp.lazy) {  // NS-base: one warp per sample streams the union of the bound lists
     if (d_bytes) throw std::invalid_argument("the B_min sector model is defined for eager plans");
     SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, nullptr};
@@ -297,6 +310,13 @@ int agpm_ns_set_strategy(int strategy) {
     if (strategy < 0 || strategy > 5)
       throw std::invalid_argument("strategy must be 0 (auto), 1 (warp), 2 (lane), 3 (frontier), 4 (fused) or 5 (flat)");
     g_strategy = strategy;
+  });
+}
+
+int agpm_ns_set_rng(int policy) {
+  return guarded([&] {
+    if (policy != 0 && policy != 1) throw std::invalid_argument("rng policy must be 0 (CounterRng) or 1 (Philox4x32-10)");
+    g_rng_policy = policy;
   });
 }
 

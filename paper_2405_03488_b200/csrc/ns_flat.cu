@@ -70,17 +70,14 @@ struct WpsOut {
   uint32_t o_pick;
 };
 
-template <int K>
+template <int K, class R>
 __device__ __noinline__ WpsOut wps_sample(const GraphArgs g, const IsectDesc<K>* dp, int lane, int src, int j,
-                                          unsigned long long key, unsigned long long ctr) {
+                                          R rr) {
   const IsectDesc<K>& d = *dp;
   const uint32_t core = d.core;
   const uint32_t nw = (d.dsize + 31) >> 5;
   unsigned long long c = 0;
   for (uint32_t w = 0; w < nw; ++w) c += __popc(live_word_g<K>(g, d, core, w, lane, j));
-  CounterRng rr(0);
-  rr.key = key;
-  rr.ctr = ctr;
   unsigned long long r = 0;
   if (lane == src && c) r = rr.next_below(c);
   r = __shfl_sync(FULL, r, src);
@@ -99,7 +96,7 @@ __device__ __noinline__ WpsOut wps_sample(const GraphArgs g, const IsectDesc<K>*
   return WpsOut{c, rr.ctr, op};
 }
 
-template <int K, int kFlatU, int kMinB>
+template <int K, int kFlatU, int kMinB, class R = CounterRng>
 __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const FrontierArgs A) {
   __shared__ IsectDesc<K> sdesc[kFlatThreads];
   __shared__ uint32_t sbal[kFlatThreads / 32][kFlatW];
@@ -116,7 +113,7 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
        base < A.count; base += stride) {
     const unsigned long long i = base + lane;
     const bool act = i < A.count;
-    Sample<K> S(A.seed, A.first_id + (act ? i : 0));
+    Sample<K, R> S(A.seed, A.first_id + (act ? i : 0));
     int pend = -1;
     if (act) {
       S.alpha = A.p.alpha0;
@@ -157,7 +154,7 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       // the r-th live element
       for (unsigned bm = __ballot_sync(FULL, wps); bm; bm &= bm - 1) {
         const int src = __ffs(bm) - 1;
-        const WpsOut o = wps_sample<K>(A.g, wdesc + src, lane, src, j, S.rng.key, S.rng.ctr);
+        const WpsOut o = wps_sample<K>(A.g, wdesc + src, lane, src, j, S.rng);
         if (lane == src) {
           cnt = o.cnt;
           o_pick = o.o_pick;
@@ -309,7 +306,7 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
   }
 }
 
-template <int K>
+template <int K, class R>
 void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
   DeviceCtx& ctx = ctx_for_current_device();
   FrontierArgs A{};
@@ -331,7 +328,7 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
   // regs 14.2 ms, 64 regs 9.1, 56 regs 8.9, 48 regs 8.8, 40 regs 9.9; triangle
   // 64 regs 5.5 vs 48 regs 5.8; 5-clique 48 regs 12.3 vs 64 regs 13.4.
   constexpr int kMinB = K == 3 ? 8 : K <= 5 ? 10 : 8;
-  auto kern = fr_flat_kernel<K, 2, kMinB>;
+  auto kern = fr_flat_kernel<K, 2, kMinB, R>;
   static int occ = -1;
   if (occ < 0) {
     int o = 0;
@@ -347,16 +344,16 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
 
 }  // namespace
 
-void launch_ns_flat(const SampleLaunch& L, cudaStream_t s) {
+void launch_ns_flat(const SampleLaunch& L, cudaStream_t s, bool philox) {
   if (L.bytes_out) throw std::invalid_argument("B_min accounting runs on the warp sampler");
   switch (L.p.k) {
-    case 3: run_flat_k<3>(L, s); break;
-    case 4: run_flat_k<4>(L, s); break;
-    case 5: run_flat_k<5>(L, s); break;
-    case 6: run_flat_k<6>(L, s); break;
-    case 7: run_flat_k<7>(L, s); break;
-    case 8: run_flat_k<8>(L, s); break;
-    case 9: run_flat_k<9>(L, s); break;
+    case 3: philox ? run_flat_k<3, PhiloxRng>(L, s) : run_flat_k<3, CounterRng>(L, s); break;
+    case 4: philox ? run_flat_k<4, PhiloxRng>(L, s) : run_flat_k<4, CounterRng>(L, s); break;
+    case 5: philox ? run_flat_k<5, PhiloxRng>(L, s) : run_flat_k<5, CounterRng>(L, s); break;
+    case 6: philox ? run_flat_k<6, PhiloxRng>(L, s) : run_flat_k<6, CounterRng>(L, s); break;
+    case 7: philox ? run_flat_k<7, PhiloxRng>(L, s) : run_flat_k<7, CounterRng>(L, s); break;
+    case 8: philox ? run_flat_k<8, PhiloxRng>(L, s) : run_flat_k<8, CounterRng>(L, s); break;
+    case 9: philox ? run_flat_k<9, PhiloxRng>(L, s) : run_flat_k<9, CounterRng>(L, s); break;
     default: throw std::invalid_argument("device sampler needs 3 <= k <= 9");
   }
 }

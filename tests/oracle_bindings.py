@@ -66,6 +66,8 @@ class Oracle:
                                                 C.POINTER(OnlineResult)]),
             "orc_exact_count": (C.c_int, graph + [C.c_int, pPlan, pu64]),
             "orc_exact_count_shard": (C.c_int, graph + [C.c_int, pPlan, u32, u32, pu64]),
+            "orc_draw_records_philox": (C.c_int, graph + [pPlan, u64, u64, u64, pdbl, pu8, pu32]),
+            "orc_philox4x32_10": (None, [pu32, u32, u32]),
             "orc_orient_by_degree": (None, [u32, pu64, pu32, pu64, pu32]),
             "orc_bernoulli_sparsify": (u64, [u32, pu64, pu32, dbl, u64, pu64, pu32]),
             "orc_triangle_count": (u64, [u32, pu64, pu32]),
@@ -121,6 +123,21 @@ class Oracle:
                                      _ptr(vals, dbl), _ptr(hits, C.c_uint8), _ptr(binds, u32))
         assert st == 0
         return vals, hits, binds
+
+    def draw_records_philox(self, off, nbr, m, plan, seed, first, count, end=None):
+        keep, (n, po, pe, pn) = self._g(off, nbr, end)
+        vals = np.zeros(count, np.float64)
+        hits = np.zeros(count, np.uint8)
+        binds = np.zeros((count, plan.k), np.uint32)
+        st = self.L.orc_draw_records_philox(n, m, po, pe, pn, C.byref(plan), seed, first, count,
+                                            _ptr(vals, dbl), _ptr(hits, C.c_uint8), _ptr(binds, u32))
+        assert st == 0
+        return vals, hits, binds
+
+    def philox4x32_10(self, ctr, key):
+        c = np.array(ctr, np.uint32)
+        self.L.orc_philox4x32_10(_ptr(c, u32), key[0], key[1])
+        return [int(x) for x in c]
 
     def fixed_budget(self, off, nbr, m, plan, budget, seed):
         keep, (n, po, pe, pn) = self._g(off, nbr)

@@ -191,3 +191,38 @@ def test_colored_exact_counts(agpm, oracle):
             colors, split, pnbr, same = oracle.color_split(off, nbr, int(c), 7)
             got = oracle.exact_count(off[:-1], pnbr, same, agpm.compile_plan(pat), end=split)
             assert got == cnt, (pat, c)
+
+
+# Philox4x32-10 known-answer vectors of the published algorithm (Salmon et al.,
+# SC'11): counter / key -> the four output words after ten rounds.
+PHILOX_KAT = [
+    ([0, 0, 0, 0], (0, 0), [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+    ([0xFFFFFFFF] * 4, (0xFFFFFFFF, 0xFFFFFFFF), [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+    ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], (0xA4093822, 0x299F31D0),
+     [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]),
+]
+
+
+@pytest.mark.parametrize("ctr,key,want", PHILOX_KAT)
+def test_philox_known_answers(oracle, ctr, key, want):
+    """The optional Philox stream's block function (oracle restatement; the
+    device copy in csrc/rng.cuh is checked against this one record for record)."""
+    assert oracle.philox4x32_10(ctr, key) == want
+
+
+def test_philox_stream_unbiased(agpm, oracle):
+    """Philox-stream NS is a valid estimator: on a small ER graph the mean of
+    2^17 samples is within 5 sigma of the exact count (the draw procedure is the
+    reference's; only the random numbers differ)."""
+    import numpy as np
+
+    g = agpm.er_graph(120, 0.15, 3)
+    off, nbr = g.arrays()
+    for pat in ("triangle", "4cycle"):
+        plan = agpm.compile_plan(pat)
+        exact = oracle.exact_count(off, nbr, g.edge_count, plan)
+        v, h, b = oracle.draw_records_philox(off, nbr, g.edge_count, plan, 11, 0, 1 << 17)
+        mu, sd = v.mean(), v.std() / np.sqrt(len(v))
+        assert abs(mu - exact) <= 5 * sd, (pat, mu, exact, sd)
+        cv, ch, cb = oracle.draw_records(off, nbr, g.edge_count, plan, 11, 0, 1 << 10)
+        assert not np.array_equal(v[: 1 << 10], cv)  # a different stream

@@ -197,3 +197,47 @@ def test_large_k_bit_exact(agpm, oracle, pattern, strat):
     assert np.count_nonzero(oh) > 0
     np.testing.assert_array_equal(v, ov)
     np.testing.assert_array_equal(b, ob)
+
+
+@pytest.mark.parametrize("name", ["er200_rel", "er60_dense", "rmat12_rel", "rmat12"])
+@pytest.mark.parametrize("pattern", ["triangle", "4clique", "5clique", "4cycle", "house", "4motif-diamond"])
+def test_philox_stream_bit_exact(agpm, oracle, graphs, name, pattern):
+    """Optional Philox4x32-10 stream (agpm_ns_set_rng(1), flat sampler): the
+    device's per-sample values, hits and bindings equal the oracle's Philox
+    restatement (whose block function passes the published known answers,
+    tests/test_cpu_oracle.py)."""
+    g = graphs[name]
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan(pattern)
+    dg = agpm.DeviceGraph(g)
+    agpm.set_rng("philox")
+    try:
+        v, h, b = agpm.draw_samples(dg, plan, 21, 5000, 6000)
+    finally:
+        agpm.set_rng("counter")
+    ov, oh, ob = oracle.draw_records_philox(off, nbr, g.edge_count, plan, 21, 5000, 6000)
+    np.testing.assert_array_equal(v, ov)
+    np.testing.assert_array_equal(b, ob)
+
+
+def test_philox_policy_errors_and_estimate(agpm, oracle):
+    g = agpm.er_graph(10000, 20 / 9999, 1).relabel_by_degree()  # config 1
+    off, nbr = g.arrays()
+    dg = agpm.DeviceGraph(g)
+    plan = agpm.compile_plan("triangle")
+    exact = agpm.exact_count(dg, plan)
+    agpm.set_rng("philox")
+    try:
+        r = agpm.run_ns_online(dg, plan, 0.01, 0.05, agpm.OnlinePolicy(), seed=3)
+        assert r.report.converged and abs(r.report.mu - exact) / exact < 0.03  # 3x the 1 % bound
+        agpm.set_strategy("frontier")
+        with pytest.raises(ValueError):
+            agpm.draw_samples(dg, plan, 1, 0, 100)
+        agpm.set_strategy("auto")
+        with pytest.raises(ValueError):
+            agpm.draw_samples(dg, agpm.compile_plan("triangle", "lazy"), 1, 0, 100)
+    finally:
+        agpm.set_rng("counter")
+        agpm.set_strategy("auto")
+    with pytest.raises(ValueError):
+        agpm.set_rng("mt19937")
