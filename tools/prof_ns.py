@@ -17,6 +17,8 @@ else:
 dg = A.DeviceGraph(g)
 plan = A.compile_plan(pattern)
 A.set_strategy(strategy)
+if os.environ.get("AGPM_RNG"):
+    A.set_rng(os.environ["AGPM_RNG"])
 B = 1 << 24
 vals = torch.empty(B, dtype=torch.float64, device="cuda")
 st = torch.cuda.Stream(); torch.cuda.set_stream(st)
