@@ -15,12 +15,17 @@ namespace {
 //     picks) runs lane-parallel, exactly as in fr_seed / fr_pick;
 //   * a multi-list step's intersection runs over the CONCATENATION of the
 //     pending samples' driver ranges: element e of the warp's flattened range
-//     goes to lane e % 32, whose sample is found from a ballot of segment
-//     starts (one redux + popc + shuffle), so lanes stay busy across sample
-//     boundaries instead of padding every sample to whole 32-element words;
+//     goes to lane e % 32, whose segment rank is found from a reduction of
+//     the segment starts (one redux + popc; the fast class reads its driver
+//     and core rows from a rank-indexed shared table), so lanes stay busy
+//     across sample boundaries instead of padding every sample to whole
+//     32-element words; fast samples (every other list a dense-core row, the
+//     driver inside the core) cost one driver load and one bit per list per
+//     element, the rest a generic per-element test;
 //   * the live ballots (32 elements per word) land in shared memory; each lane
 //     then counts its own segment, draws r = next_below(|S_j|) from its own
-//     CounterRng and selects the r-th live element — all lanes in parallel.
+//     stream (CounterRng, or the optional Philox policy) and selects the r-th
+//     live element — all lanes in parallel.
 // Drivers longer than kFlatW * 32 elements take the warp-cooperative
 // per-sample path of the fused kernel (live_word). Bound vertices inside the
 // step's [lo, hi) are failed per element (walker.hpp:70-82), so the live count
