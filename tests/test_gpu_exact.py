@@ -104,3 +104,21 @@ def test_exact_count_shards(agpm, oracle, pattern, nshards):
             agpm.exact_count(odg, plan)
     with pytest.raises(ValueError):
         agpm.exact_count_shard(dg, plan, nshards, nshards)
+
+
+
+@pytest.mark.parametrize("core", [64, 700])
+@pytest.mark.parametrize("pattern", ["triangle", "4clique", "5clique", "4cycle", "house"])
+def test_exact_partial_core(agpm, oracle, pattern, core):
+    """Leaves answered by AND-popcount of dense-core rows only where every list
+    owner and the whole range sit in the core: a core smaller than the graph
+    mixes both leaf paths; the count still equals the oracle's."""
+    g = agpm.rmat(11, 8, seed=9).relabel_by_degree()
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan(pattern)
+    agpm.set_core_dim(core)
+    try:
+        got = agpm.exact_count(agpm.DeviceGraph(g), plan)
+    finally:
+        agpm.set_core_dim(65536)
+    assert got == oracle.exact_count(off, nbr, g.edge_count, plan)

@@ -36,13 +36,15 @@ def graphs(agpm):
     return _graphs(agpm)
 
 
-@pytest.fixture(params=["warp", "lane", "frontier", "frontier_reuse", "frontier_nocore", "fused", "fused_nocore", "flat", "flat_nocore"])
+@pytest.fixture(params=["warp", "lane", "frontier", "frontier_reuse", "frontier_nocore", "fused", "fused_nocore", "flat",
+                        "flat_nocore", "flat_core96", "frontier_core96"])
 def strategy(agpm, request):
     agpm.set_strategy(request.param.split("_")[0])
     agpm.set_frontier_reuse(request.param == "frontier_reuse")
     # frontier: the dense-core bit matrix covers every vertex of the small test
-    # graphs by default; "nocore" runs the splitter-search path instead
-    agpm.set_core_dim(0 if request.param.endswith("nocore") else 65536)
+    # graphs by default; "nocore" runs the splitter-search path instead and
+    # "core96" a core of the top 96 ids only (mixed fast / generic samples)
+    agpm.set_core_dim(0 if request.param.endswith("nocore") else 96 if request.param.endswith("core96") else 65536)
     yield request.param
     agpm.set_strategy("auto")
     agpm.set_frontier_reuse(False)
