@@ -280,6 +280,17 @@ int agpm_color_split(agpm_graph* g, uint32_t colors, uint64_t seed, uint32_t* co
                      agpm_graph** out, void* stream);
 int agpm_bernoulli_sparsify(agpm_graph* g, double keep_probability, uint64_t seed, agpm_graph** out,
                             void* stream);
+/* ColoredCsr::with_colors (colored_csr.cpp:14-46): colour split of the ORIGINAL
+ * graph g for an explicit host colour array (every colour < color_count). */
+int agpm_color_split_with_colors(agpm_graph* g, const uint32_t* colors, uint32_t color_count, uint64_t* same_edges,
+                                 agpm_graph** out, void* stream);
+/* ColoredCsr::merge_colors (colored_csr.cpp:56-88): coarsen the colouring
+ * `colors` of the ORIGINAL graph g by group_map (length color_count, surjective
+ * onto a contiguous [0, c')); coarse_out (nullable, host) receives the n coarse
+ * colours. Errors: the reference's std::invalid_argument cases -> AGPM_E_INVALID. */
+int agpm_merge_colors(agpm_graph* g, const uint32_t* colors, uint32_t color_count, const uint32_t* group_map,
+                      uint32_t map_len, uint32_t* coarse_out, uint64_t* same_edges, agpm_graph** out,
+                      void* stream);
 int agpm_gs_estimate(agpm_graph* g, const agpm_plan* plan, int scheme, double keep_probability, uint32_t colors,
                      uint64_t seed, agpm_gs_result* out, void* stream);
 /* triangle_count (csr_graph.cpp:225-239) */

@@ -266,6 +266,20 @@ int ref_color_split(const RefGraph* g, uint32_t c, uint64_t seed, uint32_t* colo
   });
 }
 
+// ColoredCsr::color_vertices(c, seed).merge_colors(group_map) (colored_csr.cpp:56-88):
+// coarse colours[n], split_end[n], permuted neighbours[arcs], same-colour edges.
+int ref_merge_colors(const RefGraph* g, uint32_t c, uint64_t seed, const uint32_t* group_map, uint32_t map_len,
+                     uint32_t* colors, uint64_t* split_end, uint32_t* nbr, uint64_t* same_edges) {
+  return guard([&] {
+    ColoredCsr cc = ColoredCsr::color_vertices(g->g, c, seed)
+                        .merge_colors(std::vector<uint32_t>(group_map, group_map + map_len));
+    std::memcpy(colors, cc.colors().data(), cc.colors().size() * sizeof(uint32_t));
+    std::memcpy(split_end, cc.split_end().data(), cc.split_end().size() * sizeof(uint64_t));
+    std::memcpy(nbr, cc.base().neighbors().data(), cc.base().neighbors().size() * sizeof(uint32_t));
+    *same_edges = cc.same_color_edge_count();
+  });
+}
+
 // ---------------------------------------------------------------- NS engine
 // Per-sample records for ids [first, first+count) of stream (seed, worker, id):
 // value, hit, bindings (k per sample, 0xffffffff past a miss). Bindings come

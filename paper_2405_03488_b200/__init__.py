@@ -131,6 +131,8 @@ def _declare(L):
         "agpm_ns_set_strategy": (C.c_int, [C.c_int]),
         "agpm_exact_count": (C.c_int, [A.P, A.pPlan, A.pu64, A.P]),
         "agpm_exact_count_shard": (C.c_int, [A.P, A.pPlan, A.u32, A.u32, A.pu64, A.P]),
+        "agpm_color_split_with_colors": (C.c_int, [A.P, A.pu32, A.u32, A.pu64, C.POINTER(A.P), A.P]),
+        "agpm_merge_colors": (C.c_int, [A.P, A.pu32, A.u32, A.pu32, A.u32, A.pu32, A.pu64, C.POINTER(A.P), A.P]),
         "agpm_color_split": (C.c_int, [A.P, A.u32, A.u64, A.pu32, A.pu64, C.POINTER(A.P), A.P]),
         "agpm_bernoulli_sparsify": (C.c_int, [A.P, C.c_double, A.u64, C.POINTER(A.P), A.P]),
         "agpm_gs_estimate": (C.c_int, [A.P, A.pPlan, C.c_int, C.c_double, A.u32, A.u64, C.POINTER(A.GsResult), A.P]),
@@ -413,6 +415,28 @@ class DeviceGraph:
         h = C.c_void_p()
         _check(lib().agpm_color_split(self._h, colors, seed, _ptr(cols, C.c_uint32), C.byref(same), C.byref(h), stream))
         return DeviceGraph(_handle=h), cols[:n], same.value
+
+    def color_split_with_colors(self, colors, color_count, stream=None):
+        """ColoredCsr::with_colors -> (same-colour view, same-colour edge count)."""
+        cols = np.ascontiguousarray(colors, np.uint32)
+        same = C.c_uint64()
+        h = C.c_void_p()
+        _check(lib().agpm_color_split_with_colors(self._h, _ptr(cols, C.c_uint32), color_count, C.byref(same),
+                                                  C.byref(h), stream))
+        return DeviceGraph(_handle=h), same.value
+
+    def merge_colors(self, colors, color_count, group_map, stream=None):
+        """ColoredCsr::merge_colors of the colouring `colors` (of this graph) by group_map ->
+        (coarse same-colour view, coarse colours, same-colour edge count)."""
+        cols = np.ascontiguousarray(colors, np.uint32)
+        gm = np.ascontiguousarray(group_map, np.uint32)
+        n = self.info()["vertex_count"]
+        coarse = np.zeros(max(n, 1), np.uint32)
+        same = C.c_uint64()
+        h = C.c_void_p()
+        _check(lib().agpm_merge_colors(self._h, _ptr(cols, C.c_uint32), color_count, _ptr(gm, C.c_uint32), len(gm),
+                                       _ptr(coarse, C.c_uint32), C.byref(same), C.byref(h), stream))
+        return DeviceGraph(_handle=h), coarse[:n], same.value
 
     def bernoulli_sparsify(self, keep_probability, seed, stream=None):
         h = C.c_void_p()

@@ -8,6 +8,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <vector>
+#include <cstring>
 #include <chrono>
 #include <cmath>
 #include <stdexcept>
@@ -110,8 +112,10 @@ unsigned grid_for(uint64_t items_per_warp_n) {
 
 }  // namespace
 
-agpm_graph* color_split_device(const agpm_graph* g, uint32_t c, uint64_t seed, uint32_t* colors_host,
-                               uint64_t* same_edges, cudaStream_t s) {
+// colour split of g with colours from the seed (colour_vertices) or, with
+// explicit != null, from that host array (with_colors)
+agpm_graph* color_split_impl(const agpm_graph* g, uint32_t c, uint64_t seed, const uint32_t* explicit_host,
+                             uint32_t* colors_host, uint64_t* same_edges, cudaStream_t s) {
   if (c < 1) throw std::invalid_argument("color count must be >= 1");
   if (g->oriented) throw std::invalid_argument("colour sparsification needs the symmetric graph");
   DeviceCtx& ctx = ctx_for_current_device();
@@ -131,9 +135,13 @@ agpm_graph* color_split_device(const agpm_graph* g, uint32_t c, uint64_t seed, u
   auto* tot = static_cast<unsigned long long*>(ctx.get(3, 64));
   AGPM_CUDA(cudaMemsetAsync(tot, 0, 8, s));
   if (n) {
-    colors_kernel<<<grid_for((n + 31) / 32 * 8), 256, 0, s>>>(n, seed, c, colors);
+    if (explicit_host) {
+      AGPM_CUDA(cudaMemcpyAsync(colors, explicit_host, 4ull * n, cudaMemcpyHostToDevice, s));
+    } else {
+      colors_kernel<<<grid_for((n + 31) / 32 * 8), 256, 0, s>>>(n, seed, c, colors);
+    }
     color_split_kernel<<<grid_for(n), 256, 0, s>>>(g->vtx, g->nbr, n, colors, out->nbr, begin, split, tot);
-    count_launch(2);
+    count_launch(explicit_host ? 1 : 2);
     AGPM_CUDA(cudaGetLastError());
   }
   unsigned long long same = 0;
@@ -147,6 +155,11 @@ agpm_graph* color_split_device(const agpm_graph* g, uint32_t c, uint64_t seed, u
   AGPM_CUDA(dev_free(begin));
   AGPM_CUDA(dev_free(split));
   return out;
+}
+
+agpm_graph* color_split_device(const agpm_graph* g, uint32_t c, uint64_t seed, uint32_t* colors_host,
+                               uint64_t* same_edges, cudaStream_t s) {
+  return color_split_impl(g, c, seed, nullptr, colors_host, same_edges, s);
 }
 
 agpm_graph* bernoulli_device(const agpm_graph* g, double p, uint64_t seed, cudaStream_t s) {
@@ -196,6 +209,43 @@ int agpm_color_split(agpm_graph* g, uint32_t colors, uint64_t seed, uint32_t* co
   return guarded([&] {
     if (!g || !out) throw std::invalid_argument("null argument");
     *out = color_split_device(g, colors, seed, colors_out, same_edges, pick_stream(stream));
+  });
+}
+
+int agpm_color_split_with_colors(agpm_graph* g, const uint32_t* colors, uint32_t color_count, uint64_t* same_edges,
+                                 agpm_graph** out, void* stream) {
+  // ColoredCsr::with_colors (colored_csr.cpp:14-46): an explicit assignment
+  return guarded([&] {
+    if (!g || !out || (g->n && !colors)) throw std::invalid_argument("null argument");
+    for (uint32_t v = 0; v < g->n; ++v)
+      if (colors[v] >= color_count) throw std::invalid_argument("color out of range");
+    *out = color_split_impl(g, color_count, 0, colors, nullptr, same_edges, pick_stream(stream));
+  });
+}
+
+int agpm_merge_colors(agpm_graph* g, const uint32_t* colors, uint32_t color_count, const uint32_t* group_map,
+                      uint32_t map_len, uint32_t* coarse_out, uint64_t* same_edges, agpm_graph** out,
+                      void* stream) {
+  // ColoredCsr::merge_colors (colored_csr.cpp:56-88). Coarsening keeps each
+  // list as [same-group neighbours ascending | the rest ascending] — exactly
+  // the layout with_colors builds for the coarse colours on the original
+  // (sorted) lists, so the merged view is the colour split of the coarse map.
+  return guarded([&] {
+    if (!g || !out || !group_map || (g->n && !colors)) throw std::invalid_argument("null argument");
+    if (map_len != color_count) throw std::invalid_argument("group map must cover every color");
+    uint32_t coarse_count = 0;
+    for (uint32_t i = 0; i < map_len; ++i) coarse_count = std::max(coarse_count, group_map[i] + 1);
+    std::vector<bool> seen(coarse_count, false);
+    for (uint32_t i = 0; i < map_len; ++i) seen[group_map[i]] = true;
+    for (bool b : seen)
+      if (!b) throw std::invalid_argument("group map must be surjective onto a contiguous range");
+    std::vector<uint32_t> coarse(g->n);
+    for (uint32_t v = 0; v < g->n; ++v) {
+      if (colors[v] >= color_count) throw std::invalid_argument("color out of range");
+      coarse[v] = group_map[colors[v]];
+    }
+    if (coarse_out && g->n) std::memcpy(coarse_out, coarse.data(), 4ull * g->n);
+    *out = color_split_impl(g, coarse_count, 0, coarse.data(), nullptr, same_edges, pick_stream(stream));
   });
 }
 

@@ -268,6 +268,7 @@ class RefLib:
             "ref_graph_arrays": (None, [P, pu64, pu32]),
             "ref_triangle_count": (u64, [P]),
             "ref_color_split": (C.c_int, [P, u32, u64, pu32, pu64, pu32, pu64]),
+            "ref_merge_colors": (C.c_int, [P, u32, u64, pu32, u32, pu32, pu64, pu32, pu64]),
             "ref_draw_records": (C.c_int, [P, s, s, C.c_int, C.c_int, u64, u64, u64, u64, pdbl, pu8, pu32]),
             "ref_fixed_budget": (C.c_int, [P, s, s, C.c_int, C.c_int, u64, u64, C.c_int, pAcc]),
             "ref_ns_online": (C.c_int, [P, s, s, C.c_int, C.c_int, dbl, dbl, C.POINTER(OnlinePolicy), u64,
@@ -397,6 +398,17 @@ class RefLib:
         same = u64()
         self._chk(self.L.ref_color_split(g.h, c, seed, _ptr(colors, u32), _ptr(split, u64), _ptr(nbr, u32),
                                          C.byref(same)))
+        return colors, split, nbr[:arcs], same.value
+
+    def merge_colors(self, g, c, seed, group_map):
+        n, m, arcs, _ = g.info()
+        gm = np.asarray(group_map, np.uint32)
+        colors = np.zeros(n, np.uint32)
+        split = np.zeros(n, np.uint64)
+        nbr = np.zeros(max(arcs, 1), np.uint32)
+        same = u64()
+        self._chk(self.L.ref_merge_colors(g.h, c, seed, _ptr(gm, u32), len(gm), _ptr(colors, u32), _ptr(split, u64),
+                                          _ptr(nbr, u32), C.byref(same)))
         return colors, split, nbr[:arcs], same.value
 
     def gs_estimate(self, g, spec, scheme, p=1.0, colors=1, seed=0, threads=1, induced=""):

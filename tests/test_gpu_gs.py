@@ -89,3 +89,34 @@ def test_triangle_count(agpm, oracle):
         g = agpm.er_graph(int(n), float(p), int(s))
         assert agpm.DeviceGraph(g).triangle_count() == cnt
         assert agpm.DeviceGraph(g.orient_by_degree()).triangle_count() == cnt
+
+
+@pytest.mark.parametrize("c,seed,group_map", [(4, 19, [0, 1, 2, 3]), (4, 19, [0, 0, 0, 0]), (4, 19, [0, 0, 1, 1]),
+                                             (6, 7, [2, 0, 1, 1, 0, 2]), (5, 3, [0, 1, 0, 1, 0])])
+def test_merge_colors_matches_reference(agpm, ref, c, seed, group_map):
+    """ColoredCsr::merge_colors (colored_csr.cpp:56-88) against the compiled
+    reference: coarse colours, split ends, the permuted neighbour array and the
+    same-colour edge count are identical (identity / merge-to-one / pairwise
+    cases of test_graph_core.cpp:267-298 plus uneven maps)."""
+    g = agpm.rmat(11, 16, seed=2).relabel_by_degree()
+    off, nbr = g.arrays()
+    rg = ref.from_csr(off, nbr, g.edge_count)
+    rcol, rsplit, rnbr, rsame = ref.merge_colors(rg, c, seed, group_map)
+    dg = agpm.DeviceGraph(g)
+    _, fine, _ = dg.color_split(c, seed)
+    view, coarse, same = dg.merge_colors(fine, c, group_map)
+    b, e, nb = view.download()
+    assert np.array_equal(coarse, rcol) and np.array_equal(e, rsplit) and np.array_equal(nb, rnbr)
+    assert same == rsame == view.info()["edge_count"]
+
+
+def test_merge_colors_errors(agpm):
+    g = agpm.er_graph(40, 0.2, 3)
+    dg = agpm.DeviceGraph(g)
+    _, fine, _ = dg.color_split(4, 1)
+    with pytest.raises(ValueError):
+        dg.merge_colors(fine, 4, [0, 2, 2, 2])  # gap at 1 (test_graph_core.cpp:297)
+    with pytest.raises(ValueError):
+        dg.merge_colors(fine, 4, [0, 1])  # not total (:298)
+    with pytest.raises(ValueError):
+        dg.color_split_with_colors(np.full(40, 9, np.uint32), 4)  # colour out of range
