@@ -376,6 +376,13 @@ typedef struct agpm_region_result {
   double sparse_seconds, dense_seconds;
 } agpm_region_result;
 
+/* Colour-sparsified GS to a relative error bound: colouring
+ * i (seed derive_key(seed, i, 0), `colors` colours) is one unbiased coarse sample
+ * c^(k-1) x raw_i; the online detector (stats.cpp:57-70) stops at the first i >= 2
+ * with eps_hat <= eps, else after max_colorings. out->windows = colourings run;
+ * report / accumulator as for agpm_ns_online (sum over the X_i). */
+int agpm_gs_online(agpm_graph* g, const agpm_plan* plan, uint32_t colors, double eps, double delta,
+                   uint64_t max_colorings, uint64_t seed, agpm_online_result* out, void* stream);
 /* exact count restricted to seeds whose first vertex is < root_limit */
 int agpm_exact_count_rooted(agpm_graph* g, const agpm_plan* plan, uint32_t root_limit, uint64_t* count,
                             void* stream);

@@ -28,7 +28,7 @@ __all__ = [
     "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
     "hit_rate_report", "exact_count", "exact_count_rooted", "region_split", "gs_estimate", "choose_keep_probability", "ns_cost_cone",
     "gs_cost_estimate", "select_scheme", "count_matches_through_edge", "estimate_gamma", "fast_profile",
-    "calibrate_hardware_constant", "count_hybrid", "exact_count_shard", "bmin_bytes", "set_strategy", "set_rng", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "calibrate_hardware_constant", "count_hybrid", "exact_count_shard", "gs_online", "bmin_bytes", "set_strategy", "set_rng", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
 ]
 
@@ -131,6 +131,8 @@ def _declare(L):
         "agpm_ns_set_strategy": (C.c_int, [C.c_int]),
         "agpm_exact_count": (C.c_int, [A.P, A.pPlan, A.pu64, A.P]),
         "agpm_exact_count_shard": (C.c_int, [A.P, A.pPlan, A.u32, A.u32, A.pu64, A.P]),
+        "agpm_gs_online": (C.c_int, [A.P, A.pPlan, A.u32, C.c_double, C.c_double, A.u64, A.u64,
+                                     C.POINTER(A.OnlineResult), A.P]),
         "agpm_color_split_with_colors": (C.c_int, [A.P, A.pu32, A.u32, A.pu64, C.POINTER(A.P), A.P]),
         "agpm_merge_colors": (C.c_int, [A.P, A.pu32, A.u32, A.pu32, A.u32, A.pu32, A.pu64, C.POINTER(A.P), A.P]),
         "agpm_color_split": (C.c_int, [A.P, A.u32, A.u64, A.pu32, A.pu64, C.POINTER(A.P), A.P]),
@@ -515,6 +517,14 @@ def gs_estimate(dg, plan, scheme="color", keep_probability=1.0, colors=1, seed=0
     out = _abi.GsResult()
     _check(lib().agpm_gs_estimate(dg._h, C.byref(plan), {"bernoulli": 0, "color": 1}[scheme], keep_probability,
                                   colors, seed, C.byref(out), stream))
+    return out
+
+
+def gs_online(dg, plan, colors, eps, delta, max_colorings=4096, seed=1, stream=None):
+    """Colour GS to eps at confidence 1 - delta: one colouring per coarse sample, NS online
+    detector. OnlineResult: windows = colourings run."""
+    out = _abi.OnlineResult()
+    _check(lib().agpm_gs_online(dg._h, C.byref(plan), colors, eps, delta, max_colorings, seed, C.byref(out), stream))
     return out
 
 

@@ -237,4 +237,45 @@ int agpm_region_split(agpm_graph* g, const agpm_plan* plan, uint32_t tau_degree,
   });
 }
 
+int agpm_gs_online(agpm_graph* g, const agpm_plan* plan, uint32_t colors, double eps, double delta,
+                   uint64_t max_colorings, uint64_t seed, agpm_online_result* out, void* stream) {
+  // Colour-sparsified GS run to a relative error bound:
+  // colouring i (colours from derive_key(seed, i, 0)) gives the unbiased coarse
+  // sample X_i = c^(k-1) x raw_i (gs_engine.cpp:42-75); the X_i are i.i.d., so
+  // the NS online detector applies unchanged — accumulate (n, hits, sum, sum of
+  // squares) and stop at the first i >= 2 with eps_hat <= eps (stats.cpp:57-70),
+  // or at max_colorings.
+  return guarded([&] {
+    if (!g || !plan || !out) throw std::invalid_argument("null argument");
+    if (!(eps > 0.0) || !(eps < 1.0)) throw std::invalid_argument("error bound must be inside (0,1)");
+    if (!(delta > 0.0) || !(delta < 1.0)) throw std::invalid_argument("delta must be inside (0,1)");
+    if (colors < 1) throw std::invalid_argument("color count must be >= 1");
+    if (max_colorings < 1) throw std::invalid_argument("need at least one colouring");
+    cudaStream_t s = pick_stream(stream);
+    std::memset(out, 0, sizeof(*out));
+    agpm_accumulator acc{0, 0, 0.0, 0.0};
+    agpm_report rep{};
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t i = 0; i < max_colorings; ++i) {
+      agpm_gs_result gr{};
+      if (agpm_gs_estimate(g, plan, 1, 1.0, colors, derive_key(seed, i, 0), &gr, s) != AGPM_OK)
+        throw std::runtime_error(agpm_last_error());
+      acc.n += 1;
+      acc.hits += gr.raw_count ? 1 : 0;
+      acc.sum += gr.estimate;
+      acc.squared_sum += gr.estimate * gr.estimate;
+      if (agpm_predicted_error(&acc, delta, &rep) != AGPM_OK) throw std::runtime_error(agpm_last_error());
+      out->windows = i + 1;
+      if (rep.epsilon_hat <= eps) {
+        rep.converged = 1;
+        break;
+      }
+    }
+    out->report = rep;
+    out->accumulator = acc;
+    out->samples_launched = acc.n;
+    out->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
 }  // extern "C"
