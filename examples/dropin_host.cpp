@@ -26,6 +26,9 @@ int main(int argc, char** argv) {
   acc.add(0.0, false);
   acc.add(4.0, true);
   std::printf("eps_hat=%.5f\n", agpm::predicted_error(acc, 0.05).epsilon_hat);
+  // test_gs_engine.cpp:14-34: eps 0.1, delta 0.05, C 1e6, gamma 50 -> p = 0.05533, 18 colours
+  agpm::KeepProbability kp = agpm::choose_keep_probability({0.1, 0.05, 1e6, 50.0});
+  std::printf("keep p=%.5f colors=%u\n", kp.p, kp.color_count());
   if (device) {
     agpm::OnlineResult r = agpm::run_ns_online(g.view(), plan, 0.05, 0.05, agpm::OnlinePolicy{}, 7);
     std::printf("K4 4-cliques ~ %.4f (n=%llu converged=%d)\n", r.report.mu, (unsigned long long)r.report.n,
@@ -33,6 +36,17 @@ int main(int argc, char** argv) {
     agpm::CounterRng rng(7, 0, 3);
     agpm::SampledCount s = agpm::draw_sample(g.view(), plan, rng);
     std::printf("draw value=%.1f hit=%d\n", s.value, (int)s.hit);
+    // K4: 4 triangles, one 4-clique (test_exact_engine.cpp:19-25)
+    agpm::ExecutionPlan tri = agpm::compile_plan(agpm::parse_pattern_spec("triangle"), agpm::VerifyMode::Eager);
+    std::printf("exact triangles=%llu 4cliques=%llu\n", (unsigned long long)agpm::exact_count(g.view(), tri).count,
+                (unsigned long long)agpm::exact_count(g.view(), plan).count);
+    agpm::GsEstimate gs = agpm::gs_estimate(g, tri, agpm::SparsifyParams::color(1, 5));
+    std::printf("gs c=1 estimate=%.1f raw=%llu\n", gs.estimate, (unsigned long long)gs.raw_count);
+    agpm::ColoredCsr cc = agpm::ColoredCsr::with_colors(g, {0, 1, 0, 1}, 2);
+    agpm::ColoredCsr one = cc.merge_colors({0, 0});
+    std::printf("colored same=%llu merged same=%llu merged triangles=%llu\n",
+                (unsigned long long)cc.same_color_edge_count(), (unsigned long long)one.same_color_edge_count(),
+                (unsigned long long)one.exact_count_sparsified(tri).count);
   }
   return 0;
 }

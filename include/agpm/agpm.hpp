@@ -14,6 +14,7 @@
 // 43-45), so pointer identity identifies the data.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <list>
@@ -420,5 +421,123 @@ inline OnlineResult run_ns_online(const CsrView& g, const ExecutionPlan& plan, d
   detail::check(agpm_ns_online(detail::device_view(g), &plan.c, eps, delta, &pol, seed, &r, nullptr));
   return {detail::from_c(r.report), detail::from_c(r.accumulator), r.windows, r.work_units};
 }
+
+// ------------------------------------------------------------------ exact_engine.hpp
+struct ExactCountResult {
+  uint64_t count = 0;
+  uint64_t work_units = 0;  // not a parity target (algorithm-specific); 0 here
+};
+
+// exact_count (exact_engine.cpp:66-91); `threads` maps to the device
+inline ExactCountResult exact_count(const CsrView& g, const ExecutionPlan& plan, int /*threads*/ = 1) {
+  uint64_t c = 0;
+  detail::check(agpm_exact_count(detail::device_view(g), &plan.c, &c, nullptr));
+  return {c, 0};
+}
+
+// ------------------------------------------------------------------ csr_graph.hpp / gs_engine.hpp
+enum class SparsifyScheme { BernoulliEdge, Color };
+struct SparsifyParams {
+  SparsifyScheme scheme = SparsifyScheme::Color;
+  double keep_probability = 1.0;
+  uint32_t color_count = 1;
+  uint64_t seed = 0;
+  static SparsifyParams bernoulli(double p, uint64_t seed) { return {SparsifyScheme::BernoulliEdge, p, 1, seed}; }
+  static SparsifyParams color(uint32_t c, uint64_t seed) { return {SparsifyScheme::Color, 1.0 / c, c, seed}; }
+};
+struct GsEstimate {
+  double estimate = 0.0;
+  uint64_t raw_count = 0;
+  double scale = 1.0;
+  SparsifyParams params;
+  double preprocess_seconds = 0.0;
+  double search_seconds = 0.0;
+  uint64_t search_work_units = 0;
+};
+
+// gs_estimate (gs_engine.cpp:42-75)
+inline GsEstimate gs_estimate(const CsrGraph& g, const ExecutionPlan& plan, const SparsifyParams& params,
+                              int /*threads*/ = 1) {
+  agpm_gs_result r{};
+  detail::check(agpm_gs_estimate(detail::device_view(g.view()), &plan.c,
+                                 params.scheme == SparsifyScheme::BernoulliEdge ? 0 : 1, params.keep_probability,
+                                 params.color_count, params.seed, &r, nullptr));
+  return {r.estimate, r.raw_count, r.scale, params, r.preprocess_seconds, r.search_seconds, 0};
+}
+
+struct ReadKBoundInputs {
+  double epsilon = 0.1;
+  double delta = 0.01;
+  double count_estimate = 0.0;
+  double gamma_estimate = 1.0;
+};
+struct KeepProbability {
+  double p = 1.0;
+  bool sparsification_useless = false;
+  uint32_t color_count() const { return count_; }
+  uint32_t count_ = 1;
+};
+
+// choose_keep_probability (gs_engine.cpp:24-40)
+inline KeepProbability choose_keep_probability(const ReadKBoundInputs& in) {
+  agpm_keep_probability k{};
+  detail::check(agpm_choose_keep_probability(in.epsilon, in.delta, in.count_estimate, in.gamma_estimate, &k));
+  return {k.p, k.sparsification_useless != 0, k.color_count};
+}
+
+// ------------------------------------------------------------------ colored_csr.hpp
+// ColoredCsr on the device: the same-colour view (colored_csr.cpp:90-93) is a
+// device graph; colours and the same-colour edge count come back to the host.
+class ColoredCsr {
+ public:
+  static ColoredCsr color_vertices(const CsrGraph& g, uint32_t color_count, uint64_t seed) {
+    ColoredCsr c(g, color_count);
+    c.colors_.resize(g.vertex_count());
+    agpm_graph* v = nullptr;
+    detail::check(agpm_color_split(detail::device_view(g.view()), color_count, seed, c.colors_.data(), &c.same_,
+                                   &v, nullptr));
+    c.view_.reset(v, &agpm_graph_free);
+    return c;
+  }
+  static ColoredCsr with_colors(const CsrGraph& g, std::vector<uint32_t> colors, uint32_t color_count) {
+    ColoredCsr c(g, color_count);
+    c.colors_ = std::move(colors);
+    agpm_graph* v = nullptr;
+    detail::check(agpm_color_split_with_colors(detail::device_view(g.view()), c.colors_.data(), color_count,
+                                               &c.same_, &v, nullptr));
+    c.view_.reset(v, &agpm_graph_free);
+    return c;
+  }
+  // merge_colors (colored_csr.cpp:56-88)
+  ColoredCsr merge_colors(const std::vector<uint32_t>& group_map) const {
+    uint32_t coarse_count = 0;
+    for (uint32_t gc : group_map) coarse_count = std::max(coarse_count, gc + 1);
+    ColoredCsr c(base_, coarse_count);
+    c.colors_.resize(base_.vertex_count());
+    agpm_graph* v = nullptr;
+    detail::check(agpm_merge_colors(detail::device_view(base_.view()), colors_.data(), color_count_,
+                                    group_map.data(), static_cast<uint32_t>(group_map.size()), c.colors_.data(),
+                                    &c.same_, &v, nullptr));
+    c.view_.reset(v, &agpm_graph_free);
+    return c;
+  }
+  const std::vector<uint32_t>& colors() const { return colors_; }
+  uint32_t color_count() const { return color_count_; }
+  uint64_t same_color_edge_count() const { return same_; }
+  // exact count on the same-colour view (the raw count gs_estimate scales)
+  ExactCountResult exact_count_sparsified(const ExecutionPlan& plan) const {
+    uint64_t n = 0;
+    detail::check(agpm_exact_count(view_.get(), &plan.c, &n, nullptr));
+    return {n, 0};
+  }
+
+ private:
+  ColoredCsr(const CsrGraph& g, uint32_t c) : base_(g), color_count_(c) {}
+  CsrGraph base_;
+  uint32_t color_count_ = 1;
+  std::vector<uint32_t> colors_;
+  uint64_t same_ = 0;
+  std::shared_ptr<agpm_graph> view_;
+};
 
 }  // namespace agpm

@@ -24,6 +24,7 @@ def test_dropin_header_host_calls(agpm, tmp_path):
     assert "pattern_error ok" in out
     assert "graph n=4 m=6" in out
     assert "eps_hat=1.38590" in out  # test_ns_engine.cpp:86
+    assert "keep p=0.05533 colors=18" in out  # test_gs_engine.cpp:14-34
 
 
 @pytest.mark.gpu
@@ -33,3 +34,7 @@ def test_dropin_header_device_calls(agpm, tmp_path):
     est = float(re.search(r"K4 4-cliques ~ ([0-9.]+)", out).group(1))
     assert abs(est - 1.0) < 0.1  # K4 holds exactly one 4-clique; eps = 5 %
     assert "converged=1" in out
+    assert "exact triangles=4 4cliques=1" in out
+    assert "gs c=1 estimate=4.0 raw=4" in out
+    # colours {0,1,0,1} on K4 keep edges 0-2 and 1-3; merging both colours restores K4
+    assert "colored same=2 merged same=6 merged triangles=4" in out
