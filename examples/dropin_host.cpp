@@ -29,6 +29,10 @@ int main(int argc, char** argv) {
   // test_gs_engine.cpp:14-34: eps 0.1, delta 0.05, C 1e6, gamma 50 -> p = 0.05533, 18 colours
   agpm::KeepProbability kp = agpm::choose_keep_probability({0.1, 0.05, 1e6, 50.0});
   std::printf("keep p=%.5f colors=%u\n", kp.p, kp.color_count());
+  agpm::CostCone cone = agpm::ns_cost_cone(g.view(), plan, 1000, 1e-9);
+  agpm::GsCostEstimate gsm = agpm::gs_cost_estimate(g.view(), plan, 2, 1e-9, 4);
+  std::printf("cone %.3e..%.3e gs %.3e -> %s\n", cone.lower_time, cone.upper_time, gsm.total_seconds,
+              agpm::select_scheme(cone, gsm) == agpm::Scheme::GS ? "GS" : "NS");
   if (device) {
     agpm::OnlineResult r = agpm::run_ns_online(g.view(), plan, 0.05, 0.05, agpm::OnlinePolicy{}, 7);
     std::printf("K4 4-cliques ~ %.4f (n=%llu converged=%d)\n", r.report.mu, (unsigned long long)r.report.n,

@@ -540,4 +540,63 @@ class ColoredCsr {
   std::shared_ptr<agpm_graph> view_;
 };
 
+// ------------------------------------------------------------------ cost_model.hpp
+struct CostCone {
+  double lower_slope = 0.0;
+  double upper_slope = 0.0;
+  uint64_t n_samples = 0;
+  double lower_time = 0.0;
+  double upper_time = 0.0;
+};
+struct GsCostEstimate {
+  double preprocess_work = 0.0;
+  double search_work = 0.0;
+  double total_seconds = 0.0;
+  uint32_t color_count = 1;
+};
+struct ProfileResult {
+  double n_samples_estimate = 0.0;
+  double mu_prime = 0.0;
+  double scaled_count = 0.0;
+  double epsilon_hat_final = 0.0;
+  uint64_t n_converged = 0;
+  double fraction = 0.0;
+  bool reliable = false;
+  double seconds = 0.0;
+};
+enum class Scheme { NS, GS };
+
+// ns_cost_cone (cost_model.cpp:78-110)
+inline CostCone ns_cost_cone(const CsrView& g, const ExecutionPlan& plan, uint64_t n_samples, double hw_const) {
+  uint64_t arcs = 0;
+  for (uint32_t u = 0; u < g.vertex_count; ++u) arcs += g.end[u] - g.begin[u];
+  agpm_cost_cone c{};
+  detail::check(agpm_ns_cost_cone(g.vertex_count, static_cast<double>(arcs), &plan.c, n_samples, hw_const, &c));
+  return {c.lower_slope, c.upper_slope, c.n_samples, c.lower_time, c.upper_time};
+}
+// gs_cost_estimate (cost_model.cpp:112-145)
+inline GsCostEstimate gs_cost_estimate(const CsrView& g, const ExecutionPlan& plan, uint32_t colors, double hw_const,
+                                       uint64_t triangle_count) {
+  agpm_gs_cost c{};
+  detail::check(agpm_gs_cost_estimate(g.vertex_count, static_cast<double>(g.edge_count), &plan.c, colors, hw_const,
+                                      triangle_count, &c));
+  return {c.preprocess_work, c.search_work, c.total_seconds, c.color_count};
+}
+// fast_profile (cost_model.cpp:147-190): Bernoulli sparsification + online NS on the device
+inline ProfileResult fast_profile(const CsrGraph& g, const ExecutionPlan& plan, double profile_fraction,
+                                  double user_epsilon, uint64_t seed, int /*threads*/ = 1,
+                                  uint64_t profiler_sample_cap = 1000000) {
+  agpm_profile_result r{};
+  detail::check(agpm_fast_profile(detail::device_view(g.view()), &plan.c, profile_fraction, user_epsilon, seed,
+                                  profiler_sample_cap, &r, nullptr));
+  return {r.n_samples_estimate, r.mu_prime, r.scaled_count, r.epsilon_hat_final, r.n_converged, r.fraction,
+          r.reliable != 0, r.seconds};
+}
+// select_scheme (cost_model.cpp:192-194)
+inline Scheme select_scheme(const CostCone& cone, const GsCostEstimate& gs) {
+  const agpm_cost_cone c{cone.lower_slope, cone.upper_slope, cone.n_samples, cone.lower_time, cone.upper_time};
+  const agpm_gs_cost m{gs.preprocess_work, gs.search_work, gs.total_seconds, gs.color_count};
+  return agpm_select_scheme(&c, &m) == 1 ? Scheme::GS : Scheme::NS;
+}
+
 }  // namespace agpm

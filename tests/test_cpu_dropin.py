@@ -25,6 +25,8 @@ def test_dropin_header_host_calls(agpm, tmp_path):
     assert "graph n=4 m=6" in out
     assert "eps_hat=1.38590" in out  # test_ns_engine.cpp:86
     assert "keep p=0.05533 colors=18" in out  # test_gs_engine.cpp:14-34
+    # cost model through the header (the C entry points are reference-pinned in test_cpu_cost.py)
+    assert "cone 2.200e-05..4.700e-05 gs 2.250e-08 -> GS" in out
 
 
 @pytest.mark.gpu
