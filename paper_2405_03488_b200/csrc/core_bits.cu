@@ -59,7 +59,41 @@ __global__ void __launch_bounds__(256) core_rows_kernel(const VtxInfo* __restric
   }
 }
 
+// one thread per arc (u -> v): lower_bound of u in N(v) (u is there: symmetric view)
+__global__ void twin_kernel(const VtxInfo* __restrict__ vtx, const uint32_t* __restrict__ nbr,
+                            const unsigned long long* __restrict__ seed_arcs, unsigned long long arcs,
+                            uint32_t* __restrict__ twin) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < arcs;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long a = __ldg(seed_arcs + i);
+    const uint32_t u = (uint32_t)(a >> 32), v = (uint32_t)a;
+    const VtxInfo vv = load_vtx(vtx, v);
+    unsigned long long lo = vv.begin, hi = vv.begin + vv.deg;
+    while (lo < hi) {
+      const unsigned long long mid = (lo + hi) >> 1;
+      if (__ldg(nbr + mid) < u)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    twin[i] = (uint32_t)(lo - vv.begin);
+  }
+}
+
 }  // namespace
+
+void ensure_twin_arcs(agpm_graph* g, cudaStream_t s) {
+  if (g->twin || !g->plain || g->oriented || g->arcs == 0) return;
+  uint32_t* tw = nullptr;
+  AGPM_CUDA(dev_malloc(&tw, 4ull * g->arcs));
+  DeviceCtx& ctx = ctx_for_current_device();
+  const unsigned blocks = (unsigned)std::min<unsigned long long>((g->arcs + 255) / 256, (unsigned long long)ctx.sm_count * 16);
+  twin_kernel<<<blocks, 256, 0, s>>>(g->vtx, g->nbr, g->seed_arcs, g->arcs, tw);
+  count_launch();
+  AGPM_CUDA(cudaGetLastError());
+  g->twin = tw;
+  g->bytes += 4ull * g->arcs;
+}
 
 void set_core_dim(uint32_t dim) { g_core_dim = dim; }
 uint32_t core_dim_setting() { return g_core_dim; }

@@ -82,6 +82,7 @@ struct agpm_graph {
   uint32_t ehash_mask = 0;
   uint32_t* core = nullptr;  // dense-core bit matrix (core_bits.cu), built on demand
   uint32_t core_base = 0, core_wpr = 0, core_dim = 0;
+  uint32_t* twin = nullptr;  // twin[i] = position of u in N(v) for arc i = (u -> v); plain views, on demand
   uint64_t bytes = 0;
 };
 
@@ -96,6 +97,9 @@ void ensure_edge_hash(agpm_graph* g, cudaStream_t s);
 // build (or drop, when the configured dimension is 0) g->core for the current core dimension
 void ensure_core_bits(agpm_graph* g, cudaStream_t s);
 uint32_t core_dim_setting();
+// build g->twin if absent (plain symmetric views): the seed arc then hints
+// both seed lists
+void ensure_twin_arcs(agpm_graph* g, cudaStream_t s);
 // exact_count (exact_engine.cpp:66-91) on the device; root_limit keeps seeds whose
 // first vertex is below it, shard/nshards keep every nshards-th 32-arc chunk
 unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan, cudaStream_t s,

@@ -304,6 +304,7 @@ int agpm_graph_free(agpm_graph* g) {
     dev_free(g->seed_arcs);
     if (g->ehash) dev_free(g->ehash);
     if (g->core) dev_free(g->core);
+    if (g->twin) dev_free(g->twin);
     delete g;
   });
 }

@@ -49,6 +49,8 @@ struct GraphArgs {
   const uint32_t* __restrict__ core;
   uint32_t core_base;
   uint32_t core_wpr;
+  // twin arcs (core_bits.cu): position of u in N(v) for arc (u -> v); null = off
+  const uint32_t* __restrict__ twin;
 };
 
 // u, v >= core_base required

@@ -209,6 +209,7 @@ GraphArgs graph_args(const agpm_graph* g) {
   a.core = g->core;
   a.core_base = g->core_base;
   a.core_wpr = g->core_wpr;
+  a.twin = g->twin;
   return a;
 }
 
@@ -269,6 +270,7 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
   }
   const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, dp, count);  // B_min replay: warp kernel
   if (strat == kStrategyFrontier || strat == kStrategyFused || strat == kStrategyFlat) ensure_core_bits(const_cast<agpm_graph*>(g), s);
+  if (strat == kStrategyFrontier) ensure_twin_arcs(const_cast<agpm_graph*>(g), s);
   // (the edge-hash membership path is available but off: on RMAT-20 it turned
   // L2-local list searches into random HBM sectors and ran 2.6x slower)
   SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};

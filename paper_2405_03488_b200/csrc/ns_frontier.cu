@@ -61,12 +61,22 @@ __global__ void __launch_bounds__(256) fr_seed_kernel(const FrontierArgs A) {
     ensure_vtx(A.g, S, 0);
     ensure_vtx(A.g, S, 1);
     if (A.g.plain) {  // arc r0 is nbr[r0] in its source's list
+      // and, with twin arcs, its source sits at twin[r0] in the target's list
+      const uint32_t tw = A.g.twin ? __ldg(A.g.twin + r0) + 1 : 0u;
       if (!swapped) {
         S.hbo[0] = (uint32_t)(r0 - S.pb[0]) + 1;
         S.hbl[0] = v + 1;
+        if (tw) {  // lower_bound(v0 + 1) in N(v1)
+          S.hbo[1] = tw;
+          S.hbl[1] = u + 1;
+        }
       } else {
         S.hbo[1] = (uint32_t)(r0 - S.pb[1]) + 1;
         S.hbl[1] = u + 1;
+        if (tw) {  // lower_bound(v1 + 1) in N(v0)
+          S.hbo[0] = tw;
+          S.hbl[0] = v + 1;
+        }
       }
     }
     advance<K>(A, i, S, 0, nullptr, 0);
