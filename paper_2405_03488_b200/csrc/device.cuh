@@ -83,6 +83,7 @@ struct agpm_graph {
   uint32_t* core = nullptr;  // dense-core bit matrix (core_bits.cu), built on demand
   uint32_t core_base = 0, core_wpr = 0, core_dim = 0;
   uint32_t* twin = nullptr;  // twin[i] = position of u in N(v) for arc i = (u -> v); plain views, on demand
+  uint32_t sample_calls = 0;  // sampling launches on this view (the twin index is built on reuse)
   uint64_t bytes = 0;
 };
 

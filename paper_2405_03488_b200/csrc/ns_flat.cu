@@ -142,6 +142,10 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
         } else {
           S.hbo[1] = (uint32_t)(r0 - S.pb[1]) + 1;
           S.hbl[1] = u + 1;
+          if (A.g.twin) {  // lower_bound(v1 + 1) in N(v0) through the twin arc
+            S.hbo[0] = __ldg(A.g.twin + r0) + 1;
+            S.hbl[0] = v + 1;
+          }
         }
       }
       pend = advance<K>(A, i, S, 0, nullptr, 0, &my);
