@@ -56,6 +56,11 @@ B = 1 << 24
 WINDOW = 1000
 
 
+def config_for(n_gpus):
+    """The workload dict, identical in both arms for the same N."""
+    return dict(CONFIG, parallelism=f"samples sharded by id over {n_gpus} GPU(s)")
+
+
 def env_rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
         os.environ.get("LOCAL_RANK", "0"))
@@ -123,12 +128,8 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_rate(off, nbr, m, budget_hint, seed=1, target_s=10.0):
+def cpu_reference_rate(R, rg, budget_hint, seed=1, target_s=10.0):
     """The compiled reference's run_fixed_budget on all host cores, bounded."""
-    from oracle_bindings import RefLib
-
-    R = RefLib()
-    rg = R.from_csr(off, nbr, m)
     cores = os.cpu_count() or 1
     t = time.perf_counter()
     R.fixed_budget(rg, "4clique", 1 << 14, seed, cores)
@@ -140,20 +141,42 @@ def cpu_reference_rate(off, nbr, m, budget_hint, seed=1, target_s=10.0):
     return n / dt, cores, n, dt, acc
 
 
+def cpu_reference_ttc(R, rg, seed=1):
+    """run_ns_online(view, 4clique eager, 0.01, 0.05, OnlinePolicy{}, seed, nproc) on the
+    host cores, wall time from the resident graph to the report."""
+    from paper_2405_03488_b200._abi import OnlinePolicy
+
+    cores = os.cpu_count() or 1
+    t = time.perf_counter()
+    r = R.ns_online(rg, "4clique", 0.01, 0.05, OnlinePolicy(), seed, cores)
+    dt = time.perf_counter() - t
+    return {"seconds": dt, "samples": r.report.n, "windows": r.windows, "estimate": r.report.mu,
+            "epsilon_hat": r.report.epsilon_hat, "converged": bool(r.report.converged), "workers": cores,
+            "note": "reference streams keyed (seed, worker, index) with workers = nproc"}
+
+
+def reference_host():
+    from oracle_bindings import cpu_model, timing_ref_so
+
+    path, flags = timing_ref_so()
+    return path, {"cpu_model": cpu_model(), "nproc": os.cpu_count(), "build": flags,
+                  "library": os.path.relpath(path, ROOT)}
+
+
 def run_reference(args):
+    """The reference's own CPU implementation of the path (oracle/_ref: the
+    unmodified reference sources compiled here), on the host cores. Its input is
+    built without the product library: oracle generator -> reference
+    CsrGraph::from_edges -> oracle relabel -> AGPM v1 -> reference load_graph_auto."""
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    import numpy as np  # noqa: F401
+    from oracle_bindings import reference_rmat_graph
 
-    import paper_2405_03488_b200 as A
-    from oracle_bindings import RefLib
-
-    g = make_graph(A)
-    off, nbr = g.arrays()
-    m = g.edge_count
-    R = RefLib()
-    rg = R.from_csr(off, nbr, m)
+    path, host = reference_host()
+    t0 = time.perf_counter()
+    R, rg = reference_rmat_graph(20, 16, 0.57, 0.19, 0.19, seed=1, ref_path=path)
+    build_s = time.perf_counter() - t0
     cores = os.cpu_count() or 1
     # bound each step to ~3 s of CPU work
     t = time.perf_counter()
@@ -167,14 +190,21 @@ def run_reference(args):
         R.fixed_budget(rg, "4clique", per_step, 1 + s, cores)
     el = time.perf_counter() - t
     value = per_step * args.steps / el
+    ttc = cpu_reference_ttc(R, rg, seed=1)
+    n, m, arcs, _ = rg.info()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * el / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64",
-        "data": "synthetic", "config": dict(CONFIG, samples_per_step=per_step),
+        "data": "synthetic (seeded RMAT generator, no dataset)", "config": config_for(args.gpus),
+        "time_to_converge": ttc,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{per_step} samples/step of the workload, run_fixed_budget(workers={cores})"},
+                         "sample": f"{per_step} samples/step of the workload, run_fixed_budget(workers={cores})",
+                         **host},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "graph_stats": {"n": n, "m": m, "arcs": arcs, "build_s": round(build_s, 2),
+                        "input": "oracle generator + reference from_edges + oracle relabel + "
+                                 "reference load_graph_auto (no product code)"},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -338,30 +368,48 @@ def run_gpu(args):
                "epsilon_hat": rp.epsilon_hat, "hit_rate": rp.hit_rate, "converged": bool(rp.converged),
                "ranks": world, "samples_per_rank_per_batch": per_rank}
     elif rank == 0:
+        # cold view: a fresh device view (upload untimed), so the run includes the
+        # one-time dense-core matrix and twin-arc index builds
+        dg_cold = A.DeviceGraph(g, stream=sptr)
+        torch.cuda.synchronize()
+        rc = A.run_ns_online(dg_cold, plan, 0.01, 0.05, A.OnlinePolicy(), seed=1)
+        del dg_cold
         A.run_ns_online(dg, plan, 0.01, 0.05, A.OnlinePolicy(), seed=1)
         r = A.run_ns_online(dg, plan, 0.01, 0.05, A.OnlinePolicy(), seed=1)
-        ttc = {"seconds": r.seconds, "samples": r.report.n, "windows": r.windows,
+        assert (rc.report.n, rc.accumulator.hits) == (r.report.n, r.accumulator.hits)
+        ttc = {"seconds": r.seconds, "seconds_cold_view": rc.seconds, "samples": r.report.n, "windows": r.windows,
                "samples_launched": r.samples_launched, "estimate": r.report.mu,
                "epsilon_hat": r.report.epsilon_hat, "hit_rate": r.report.hit_rate,
-               "converged": bool(r.report.converged)}
+               "converged": bool(r.report.converged),
+               "note": "seconds: view already indexed (dense core + twin arcs built); seconds_cold_view: "
+                       "first run on a fresh view, index builds included"}
 
     peak, peak_src = peaks()
     achieved = bmin_per_sample * B / (kern_ms / 1000.0) / 1e9
     traffic = None
+    traffic_src = "no ncu capture on record for this workload"
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
         if tr.get("workload") == CONFIG["workload"] and tr.get("samples_per_launch") == B:
             traffic = tr["dram_bytes_per_launch"]
+            traffic_src = f"profile value, not measured in this run: {tr.get('source', 'profiles/ncu_traffic.json')}"
     except Exception:
         pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rate, cores, n, dt, _ = cpu_reference_rate(off, nbr, m, 1 << 22)
+            from oracle_bindings import RefLib
+
+            path, host = reference_host()
+            R = RefLib(path)
+            rg = R.from_csr(off, nbr, m)
+            rate, cores, n, dt, _ = cpu_reference_rate(R, rg, 1 << 22)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
-                   "sample": f"{n} samples of the same workload (run_fixed_budget, workers={cores}) in {dt:.1f} s"}
+                   "sample": f"{n} samples of the same workload (run_fixed_budget, workers={cores}) in {dt:.1f} s",
+                   "time_to_converge": cpu_reference_ttc(R, rg, seed=1), **host}
+            del rg, R
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -371,9 +419,9 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic (seeded RMAT generator, no dataset)",
-            "config": dict(CONFIG, parallelism=f"samples sharded by id over {world} GPU(s)",
-                           graph_stats={"n": info["vertex_count"], "m": info["edge_count"],
-                                        "device_bytes": info["device_bytes"], "gen_s": round(gen_s, 2)}),
+            "config": config_for(world),
+            "graph_stats": {"n": info["vertex_count"], "m": info["edge_count"], "device_bytes": info["device_bytes"],
+                            "gen_s": round(gen_s, 2)},
             "time_to_converge": ttc,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "what": "DeviceGraph(pinned host CSR) upload + device view build + run_fixed_budget(2^24) + "
@@ -381,7 +429,8 @@ def run_gpu(args):
                     "upload_s_per_step": up_s / e2e_steps, "sampling_s_per_step": run_s / e2e_steps,
                     "upload_ms": up_list, "sampling_ms": run_list},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
                          "bmin_bytes_per_sample": bmin_per_sample, "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / ms_per_step},
             "cpu_baseline": cpu,

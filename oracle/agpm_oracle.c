@@ -587,6 +587,90 @@ int orc_ns_online(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t*
   return AGPM_OK;
 }
 
+/* Multi-threaded checker variants for the big configs (RMAT-22 … RMAT-26 parity
+ * tests): each sample is still drawn by draw_one from its own stream
+ * CounterRng(seed, 0, i), so per-sample records are those of the sequential
+ * functions above; the online run draws a speculative block of windows in
+ * parallel into a value buffer, then accumulates it SEQUENTIALLY in sample-id
+ * order with the stop test after every window — bit-identical to
+ * orc_ns_online (ns_engine.cpp:106-140 with workers = 1), only faster. */
+int orc_draw_records_mt(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t* end,
+                        const uint32_t* nbr, const agpm_plan* plan, uint64_t seed, uint64_t first,
+                        uint64_t count, double* values, uint8_t* hits, uint32_t* bindings, int threads) {
+  view_t g = mkview(n, m, begin, end, nbr, 0);
+  if (g.m == 0) return AGPM_E_INVALID;
+  seed_index_t si = seed_index(&g);
+  const int64_t chunk = 256;
+  const int64_t nchunks = (int64_t)((count + chunk - 1) / chunk);
+#pragma omp parallel num_threads(threads > 0 ? threads : 1)
+  {
+    scratch_t s = {{0, 0, 0}, {0, 0, 0}};
+    uint32_t b[AGPM_MAX_K];
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t c = 0; c < nchunks; ++c) {
+      uint64_t lo = (uint64_t)c * chunk, hi = lo + chunk < count ? lo + chunk : count;
+      for (uint64_t i = lo; i < hi; ++i) {
+        orc_rng rng = rng_make(seed, 0, first + i);
+        double val;
+        int nb = draw_one(&g, &si, plan, &rng, b, &val, &s);
+        values[i] = val;
+        hits[i] = val != 0.0;
+        if (bindings)
+          for (int p = 0; p < plan->k; ++p) bindings[i * plan->k + p] = p < nb ? b[p] : 0xffffffffu;
+      }
+    }
+    free(s.out.d);
+    free(s.tmp.d);
+  }
+  free(si.prefix);
+  return AGPM_OK;
+}
+
+int orc_ns_online_mt(uint32_t n, uint64_t m, const uint64_t* begin, const uint64_t* end,
+                     const uint32_t* nbr, const agpm_plan* plan, double eps, double delta,
+                     const agpm_online_policy* pol, uint64_t seed, agpm_online_result* out, int threads) {
+  if (!(eps > 0.0) || !(eps < 1.0) || !(delta > 0.0) || !(delta < 1.0)) return AGPM_E_INVALID;
+  view_t g = mkview(n, m, begin, end, nbr, 0);
+  if (g.m == 0) return AGPM_E_INVALID;
+  uint64_t window = pol->n_min > 10 ? pol->n_min : 10;
+  if (pol->profiled_n_samples > 0 && pol->profiled_n_samples / 10 > window)
+    window = pol->profiled_n_samples / 10;
+  const uint64_t block = 1ull << 17; /* samples drawn speculatively per round */
+  double* vals = (double*)malloc(block * sizeof(double));
+  uint8_t* hit = (uint8_t*)malloc(block);
+  memset(out, 0, sizeof(*out));
+  agpm_accumulator acc = {0, 0, 0.0, 0.0};
+  uint64_t drawn = 0, idx = 0, have = 0, used = 0; /* buffer holds ids [idx-have, idx) */
+  int done = 0;
+  while (!done) {
+    uint64_t this_window = pol->max_samples - drawn < window ? pol->max_samples - drawn : window;
+    if (this_window == 0) break;
+    for (uint64_t i = 0; i < this_window; ++i) {
+      if (used == have) {
+        orc_draw_records_mt(n, m, begin, end, nbr, plan, seed, idx, block, vals, hit, NULL, threads);
+        idx += block;
+        have = block;
+        used = 0;
+      }
+      acc_add(&acc, vals[used], hit[used]);
+      ++used;
+    }
+    drawn += this_window;
+    ++out->windows;
+    orc_predicted_error(&acc, delta, &out->report);
+    out->accumulator = acc;
+    if (out->report.epsilon_hat <= eps) {
+      out->report.converged = 1;
+      done = 1;
+    } else if (drawn >= pol->max_samples) {
+      done = 1;
+    }
+  }
+  free(vals);
+  free(hit);
+  return AGPM_OK;
+}
+
 /* ------------------------------------------------------------ exact_engine.cpp:19-91 */
 /* exact_engine.cpp:19-62 search_from_seed: the iterative DFS restated recursively */
 static uint64_t dfs(const view_t* g, const agpm_plan* plan, int apply_bounds, uint32_t* binding,
@@ -725,4 +809,86 @@ uint64_t orc_color_split(uint32_t n, const uint64_t* off, const uint32_t* nbr, u
       if (colors[nbr[e]] != colors[u]) out_nbr[w++] = nbr[e];
   }
   return same / 2;
+}
+
+/* ------------------------------------------------------------ benchmark graph inputs */
+/* The reference arm of bench.py builds its input without the product library:
+ * edges from this generator, CSR by the reference's own CsrGraph::from_edges,
+ * the (degree, id) relabel below, the AGPM v1 file below, then the reference's
+ * load_graph_auto. tests/test_cpu_oracle.py pins the result to the product's
+ * rmat(...).relabel_by_degree() array for array. */
+
+/* The benchmark RMAT generator (the product's definition, csrc/host_graph.cpp
+ * gen_rmat): edge i draws `scale` doubles from
+ * CounterRng(seed, "rmat", i) (rng.hpp:28-37) and descends the quadrants
+ * (a | b: v bit | c: u bit | d: both), bits appended MSB first. pairs = 2*ef<<scale u32. */
+void orc_gen_rmat_pairs(uint32_t scale, uint32_t edge_factor, double a, double b, double c, uint64_t seed,
+                        uint32_t* pairs) {
+  const int64_t m = (int64_t)edge_factor << scale;
+  const double ab = a + b, abc = a + b + c;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; ++i) {
+    orc_rng r = rng_make(seed, 0x726d6174ull /* "rmat" */, (uint64_t)i);
+    uint32_t u = 0, v = 0;
+    for (uint32_t l = 0; l < scale; ++l) {
+      double x = rng_double(&r);
+      uint32_t bu = x >= ab, bv = (x >= a && x < ab) || x >= abc;
+      u = (u << 1) | bu;
+      v = (v << 1) | bv;
+    }
+    pairs[2 * i] = u;
+    pairs[2 * i + 1] = v;
+  }
+}
+
+static int cmp_u32(const void* x, const void* y) {
+  uint32_t a = *(const uint32_t*)x, b = *(const uint32_t*)y;
+  return (a > b) - (a < b);
+}
+
+/* Relabel by (degree, id) rank (not in the reference —
+ * the product's definition, csrc/host_graph.cpp relabel_by_degree): a stable
+ * counting sort by degree gives order[]; vertex order[i] becomes i; each new
+ * list is the old list mapped and sorted ascending. out_off n+1, out_nbr arcs. */
+void orc_relabel_by_degree(uint32_t n, const uint64_t* off, const uint32_t* nbr, uint64_t* out_off,
+                           uint32_t* out_nbr) {
+  uint64_t maxd = 0;
+  for (uint32_t u = 0; u < n; ++u)
+    if (off[u + 1] - off[u] > maxd) maxd = off[u + 1] - off[u];
+  uint64_t* bucket = (uint64_t*)calloc(maxd + 2, sizeof(uint64_t));
+  uint32_t* order = (uint32_t*)malloc((size_t)n * sizeof(uint32_t) + 4);
+  uint32_t* new_id = (uint32_t*)malloc((size_t)n * sizeof(uint32_t) + 4);
+  for (uint32_t u = 0; u < n; ++u) ++bucket[off[u + 1] - off[u] + 1];
+  for (uint64_t d = 1; d <= maxd + 1; ++d) bucket[d] += bucket[d - 1];
+  for (uint32_t u = 0; u < n; ++u) order[bucket[off[u + 1] - off[u]]++] = u;
+  for (uint32_t i = 0; i < n; ++i) new_id[order[i]] = i;
+  out_off[0] = 0;
+  for (uint32_t i = 0; i < n; ++i) out_off[i + 1] = out_off[i] + (off[order[i] + 1] - off[order[i]]);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t i = 0; i < (int64_t)n; ++i) {
+    const uint32_t old = order[i];
+    uint32_t* dst = out_nbr + out_off[i];
+    const uint64_t d = off[old + 1] - off[old];
+    for (uint64_t j = 0; j < d; ++j) dst[j] = new_id[nbr[off[old] + j]];
+    qsort(dst, d, sizeof(uint32_t), cmp_u32);
+  }
+  free(bucket);
+  free(order);
+  free(new_id);
+}
+
+/* write_binary_csr (csr_graph.cpp, the AGPM v1 layout): "AGPM", u32 version 1,
+ * u64 n, u64 m, u64 offsets[n+1], u32 neighbors[offsets[n]], little endian
+ * (this host is little endian, so the arrays are written as they lie). */
+#include <stdio.h>
+int orc_write_binary_csr(const char* path, uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr) {
+  FILE* f = fopen(path, "wb");
+  if (!f) return AGPM_E_IO;
+  const uint32_t version = 1;
+  const uint64_t n64 = n;
+  int ok = fwrite("AGPM", 1, 4, f) == 4 && fwrite(&version, 4, 1, f) == 1 && fwrite(&n64, 8, 1, f) == 1 &&
+           fwrite(&m, 8, 1, f) == 1 && fwrite(off, 8, (size_t)n + 1, f) == (size_t)n + 1 &&
+           fwrite(nbr, 4, off[n], f) == off[n];
+  ok = (fclose(f) == 0) && ok;
+  return ok ? AGPM_OK : AGPM_E_IO;
 }

@@ -21,6 +21,34 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_DIR = os.path.join(ROOT, "oracle")
 ORACLE_SO = os.path.join(ORACLE_DIR, "liboracle.so")
 REF_SO = os.path.join(ORACLE_DIR, "_ref", "libagpm_ref.so")
+# the timing build of the same sources (-O3 -DNDEBUG -march=x86-64-v3, oracle/Makefile)
+REF_FAST_SO = os.path.join(ORACLE_DIR, "_ref", "libagpm_ref_fast.so")
+REF_FAST_FLAGS = "g++ -O3 -DNDEBUG -march=x86-64-v3 -fopenmp -std=c++20"
+REF_FLAGS = "g++ -O3 -fopenmp -std=c++20 (the reference CMake Release flags)"
+
+
+def cpu_has_x86_64_v3():
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = next((ln for ln in f if ln.startswith("flags")), "").split()
+        return all(x in flags for x in ("avx2", "bmi2", "fma", "movbe"))
+    except OSError:
+        return False
+
+
+def timing_ref_so():
+    """(path, flags) of the reference build bench.py times on this host."""
+    if os.path.exists(REF_FAST_SO) and cpu_has_x86_64_v3():
+        return REF_FAST_SO, REF_FAST_FLAGS
+    return REF_SO, REF_FLAGS
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            return next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "unknown")
+    except OSError:
+        return "unknown"
 
 u32, u64, dbl, P = C.c_uint32, C.c_uint64, C.c_double, C.c_void_p
 pu32, pu64, pdbl, pu8 = C.POINTER(u32), C.POINTER(u64), C.POINTER(dbl), C.POINTER(C.c_uint8)
@@ -67,7 +95,13 @@ class Oracle:
             "orc_exact_count": (C.c_int, graph + [C.c_int, pPlan, pu64]),
             "orc_exact_count_shard": (C.c_int, graph + [C.c_int, pPlan, u32, u32, pu64]),
             "orc_draw_records_philox": (C.c_int, graph + [pPlan, u64, u64, u64, pdbl, pu8, pu32]),
+            "orc_draw_records_mt": (C.c_int, graph + [pPlan, u64, u64, u64, pdbl, pu8, pu32, C.c_int]),
+            "orc_ns_online_mt": (C.c_int, graph + [pPlan, dbl, dbl, C.POINTER(OnlinePolicy), u64,
+                                                   C.POINTER(OnlineResult), C.c_int]),
             "orc_philox4x32_10": (None, [pu32, u32, u32]),
+            "orc_gen_rmat_pairs": (None, [u32, u32, dbl, dbl, dbl, u64, pu32]),
+            "orc_relabel_by_degree": (None, [u32, pu64, pu32, pu64, pu32]),
+            "orc_write_binary_csr": (C.c_int, [C.c_char_p, u32, u64, pu64, pu32]),
             "orc_orient_by_degree": (None, [u32, pu64, pu32, pu64, pu32]),
             "orc_bernoulli_sparsify": (u64, [u32, pu64, pu32, dbl, u64, pu64, pu32]),
             "orc_triangle_count": (u64, [u32, pu64, pu32]),
@@ -123,6 +157,26 @@ class Oracle:
                                      _ptr(vals, dbl), _ptr(hits, C.c_uint8), _ptr(binds, u32))
         assert st == 0
         return vals, hits, binds
+
+    def draw_records_mt(self, off, nbr, m, plan, seed, first, count, end=None, threads=None):
+        """draw_records over all host cores (same records: one stream per sample id)."""
+        keep, (n, po, pe, pn) = self._g(off, nbr, end)
+        vals = np.zeros(count, np.float64)
+        hits = np.zeros(count, np.uint8)
+        binds = np.zeros((count, plan.k), np.uint32)
+        st = self.L.orc_draw_records_mt(n, m, po, pe, pn, C.byref(plan), seed, first, count, _ptr(vals, dbl),
+                                        _ptr(hits, C.c_uint8), _ptr(binds, u32), threads or os.cpu_count() or 1)
+        assert st == 0
+        return vals, hits, binds
+
+    def ns_online_mt(self, off, nbr, m, plan, eps, delta, policy, seed, end=None, threads=None):
+        """ns_online with the samples drawn on all host cores; accumulation and stop
+        test sequential in id order, so the result is ns_online's bit for bit."""
+        keep, (n, po, pe, pn) = self._g(off, nbr, end)
+        res = OnlineResult()
+        assert self.L.orc_ns_online_mt(n, m, po, pe, pn, C.byref(plan), eps, delta, C.byref(policy), seed,
+                                       C.byref(res), threads or os.cpu_count() or 1) == 0
+        return res
 
     def draw_records_philox(self, off, nbr, m, plan, seed, first, count, end=None):
         keep, (n, po, pe, pn) = self._g(off, nbr, end)
@@ -180,6 +234,27 @@ class Oracle:
                                       _ptr(split, u64), _ptr(out, u32))
         return colors, split, out, same
 
+    def rmat_pairs(self, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1):
+        """The benchmark RMAT edge list ((ef << scale), 2) u32 — the product generator restated."""
+        pairs = np.empty(((edge_factor << scale), 2), np.uint32)
+        self.L.orc_gen_rmat_pairs(scale, edge_factor, a, b, c, seed, _ptr(pairs, u32))
+        return pairs
+
+    def relabel_by_degree(self, off, nbr):
+        off = np.ascontiguousarray(off, dtype=np.uint64)
+        nbr = np.ascontiguousarray(nbr, dtype=np.uint32)
+        n = len(off) - 1
+        o_off = np.zeros(n + 1, np.uint64)
+        o_nbr = np.zeros(max(len(nbr), 1), np.uint32)
+        self.L.orc_relabel_by_degree(n, _ptr(off, u64), _ptr(nbr, u32), _ptr(o_off, u64), _ptr(o_nbr, u32))
+        return o_off, o_nbr[: len(nbr)]
+
+    def write_binary_csr(self, path, off, nbr, m):
+        off = np.ascontiguousarray(off, dtype=np.uint64)
+        nbr = np.ascontiguousarray(nbr, dtype=np.uint32)
+        if self.L.orc_write_binary_csr(_b(path), len(off) - 1, m, _ptr(off, u64), _ptr(nbr, u32)) != 0:
+            raise OSError(f"cannot write {path}")
+
     def triangle_count(self, off, nbr):
         off = np.ascontiguousarray(off, dtype=np.uint64)
         nbr = np.ascontiguousarray(nbr, dtype=np.uint32)
@@ -231,10 +306,11 @@ class RefLib:
 
     available = os.path.exists(REF_SO)
 
-    def __init__(self):
-        if not os.path.exists(REF_SO):
-            raise FileNotFoundError(REF_SO)
-        L = C.CDLL(REF_SO)
+    def __init__(self, path=None):
+        path = path or REF_SO
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = C.CDLL(path)
         ph = C.POINTER(P)
         s = C.c_char_p
         sig = {
@@ -419,3 +495,29 @@ class RefLib:
 
     def triangle_count(self, g):
         return self.L.ref_triangle_count(g.h)
+
+
+def reference_rmat_graph(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, path=None, ref_path=None):
+    """The benchmark RMAT graph built WITHOUT the product library (bench.py's
+    reference arm): edges from the oracle's generator restatement, CSR from the
+    reference's own CsrGraph::from_edges (csr_graph.cpp:46-72), the oracle's
+    (degree, id) relabel, written as AGPM v1 and read back through the
+    reference's load_graph_auto (csr_graph.cpp:143-170). Returns (RefLib, RefGraph)."""
+    import tempfile
+
+    O, R = Oracle(), RefLib(ref_path)
+    g0 = R.from_edges(O.rmat_pairs(scale, edge_factor, a, b, c, seed), 1 << scale)
+    m = g0.info()[1]
+    off, nbr = O.relabel_by_degree(*g0.arrays())
+    del g0
+    own = path is None
+    if own:
+        fd, path = tempfile.mkstemp(suffix=".agpm")
+        os.close(fd)
+    try:
+        O.write_binary_csr(path, off, nbr, m)
+        del off, nbr
+        return R, R.load(path)
+    finally:
+        if own:
+            os.unlink(path)

@@ -226,3 +226,40 @@ def test_philox_stream_unbiased(agpm, oracle):
         assert abs(mu - exact) <= 5 * sd, (pat, mu, exact, sd)
         cv, ch, cb = oracle.draw_records(off, nbr, g.edge_count, plan, 11, 0, 1 << 10)
         assert not np.array_equal(v[: 1 << 10], cv)  # a different stream
+
+
+def test_multithreaded_checker_equals_sequential(agpm, oracle):
+    """The parallel checker variants used by the big-config parity tests
+    (orc_draw_records_mt, orc_ns_online_mt) give the sequential oracle's results
+    bit for bit: records per sample id, online stop n, hits and the in-order sums."""
+    g = agpm.rmat(11, 16, seed=5).relabel_by_degree()
+    off, nbr = g.arrays()
+    for spec in ("4clique", "4cycle", "triangle"):
+        plan = agpm.compile_plan(spec)
+        for first in (0, 1 << 40):
+            a = oracle.draw_records(off, nbr, g.edge_count, plan, 3, first, 3000)
+            b = oracle.draw_records_mt(off, nbr, g.edge_count, plan, 3, first, 3000, threads=4)
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y), spec
+        pol = OnlinePolicy()
+        s = oracle.ns_online(off, nbr, g.edge_count, plan, 0.02, 0.05, pol, 7)
+        p = oracle.ns_online_mt(off, nbr, g.edge_count, plan, 0.02, 0.05, pol, 7, threads=4)
+        assert (s.report.n, s.windows, s.accumulator.hits) == (p.report.n, p.windows, p.accumulator.hits)
+        assert s.accumulator.sum.hex() == p.accumulator.sum.hex()
+        assert s.accumulator.squared_sum.hex() == p.accumulator.squared_sum.hex()
+        assert s.report.epsilon_hat.hex() == p.report.epsilon_hat.hex()
+
+
+def test_reference_arm_graph_equals_product_graph(agpm, ref):
+    """bench.py's reference arm builds its RMAT input with no product code
+    (oracle generator -> reference from_edges -> oracle relabel -> AGPM v1 ->
+    reference load_graph_auto); it must be the product's graph array for array."""
+    from oracle_bindings import reference_rmat_graph
+
+    for scale, ef, seed in ((10, 16, 1), (13, 8, 5)):
+        _, rg = reference_rmat_graph(scale, ef, seed=seed)
+        off, nbr = rg.arrays()
+        g = agpm.rmat(scale, ef, 0.57, 0.19, 0.19, seed=seed).relabel_by_degree()
+        poff, pnbr = g.arrays()
+        assert np.array_equal(off, poff) and np.array_equal(nbr, pnbr)
+        assert rg.info()[1] == g.edge_count

@@ -1,0 +1,130 @@
+"""GPU parity at the big configs' own scale (BASELINE.json configs 3 and 5).
+
+The samplers that only run on big graphs — the frontier phases (non-clique
+plans; clique plans once n > 64 x the dense-core dimension), hub-list
+(long-driver) paths, the partial dense core, the twin-arc hints (built on a
+view's second sampling launch) — are pinned here against the oracle on the
+graphs themselves, not on scaled-down stand-ins:
+
+* config 3: RMAT-22 ef16 relabelled, 4-cycle (+ 4-clique on the flat and
+  frontier samplers);
+* config 5 class: RMAT-25 ef16 relabelled, 4-clique (n = 2^25 > 64 x 65 536, so
+  the auto strategy is the frontier), and RMAT-27 itself when the host can hold
+  the oracle's copy of the 4.2 B-arc CSR.
+
+Each graph is built on the device (== the host builders, tests/test_gpu_ingest.py)
+and downloaded for the oracle, so both sides read the same arrays. Per-sample
+records (value bits, hit, bindings) are compared at three id offsets (0, 2^30,
+2^40), and run_ns_online(1 %, 5 %) must stop at the oracle's n with its hits and
+sums (ns_engine.cpp:27-53, 106-140). The oracle runs its multi-threaded
+variants (orc_draw_records_mt / orc_ns_online_mt: same streams, in-order
+accumulation — bit-identical to the sequential functions, test_cpu_oracle.py).
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+OFFSETS = (0, 1 << 30, 1 << 40)
+COUNT = 1 << 18  # >= 2^18: the batch size where the auto strategy leaves the warp sampler
+STRATEGY = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3, "flat": 5}
+
+
+def _graph(agpm, scale):
+    dg = agpm.rmat_device(scale, 16, 0.57, 0.19, 0.19, seed=1, relabel=True)
+    b, e, nb = dg.download()
+    return dg, (b, e, nb), dg.info()
+
+
+def _records_equal(agpm, oracle, dg, host, m, plan, first, count):
+    b, e, nb = host
+    v, h, bd = agpm.draw_samples(dg, plan, 1, first, count)
+    ov, oh, ob = oracle.draw_records_mt(b, nb, m, plan, 1, first, count, end=e)
+    bad = np.flatnonzero((v.view(np.uint64) != ov.view(np.uint64)) | (h != oh) | (bd != ob).any(axis=1))
+    assert bad.size == 0, (f"{bad.size} of {count} records differ from the oracle at id offset {first}; "
+                           f"first id {first + int(bad[0])}: device {v[bad[0]]!r} {bd[bad[0]].tolist()} "
+                           f"oracle {ov[bad[0]]!r} {ob[bad[0]].tolist()}")
+    return int(h.sum())
+
+
+def _online_equal(agpm, oracle, dg, host, m, plan):
+    b, e, nb = host
+    pol = agpm.OnlinePolicy()
+    r = agpm.run_ns_online(dg, plan, 0.01, 0.05, pol, seed=1)
+    o = oracle.ns_online_mt(b, nb, m, plan, 0.01, 0.05, pol, 1, end=e)
+    assert r.report.converged and o.report.converged
+    assert (r.report.n, r.windows, r.accumulator.hits) == (o.report.n, o.windows, o.accumulator.hits)
+    assert abs(r.accumulator.sum - o.accumulator.sum) <= 1e-12 * o.accumulator.sum
+    assert abs(r.accumulator.squared_sum - o.accumulator.squared_sum) <= 1e-12 * o.accumulator.squared_sum
+    return r
+
+
+@pytest.fixture(scope="module")
+def rmat22(agpm):
+    return _graph(agpm, 22)
+
+
+@pytest.mark.parametrize("spec,strategy", [("4cycle", "auto"), ("4clique", "auto"), ("4clique", "frontier"),
+                                           ("4cycle", "warp"), ("triangle", "auto")])
+def test_config3_records(agpm, oracle, rmat22, spec, strategy):
+    dg, host, info = rmat22
+    plan = agpm.compile_plan(spec)
+    agpm.set_strategy(strategy)
+    try:
+        hits = [_records_equal(agpm, oracle, dg, host, info["edge_count"], plan, f, COUNT) for f in OFFSETS]
+    finally:
+        agpm.set_strategy("auto")
+    assert sum(hits) > 0
+
+
+def test_config3_online(agpm, oracle, rmat22):
+    dg, host, info = rmat22
+    r = _online_equal(agpm, oracle, dg, host, info["edge_count"], agpm.compile_plan("4cycle"))
+    assert r.report.n >= 1000
+
+
+@pytest.fixture(scope="module")
+def rmat25(agpm):
+    return _graph(agpm, 25)
+
+
+@pytest.mark.parametrize("spec,strategy", [("4clique", "auto"), ("4clique", "flat"), ("4cycle", "auto")])
+def test_config5_class_records(agpm, oracle, rmat25, spec, strategy):
+    dg, host, info = rmat25
+    assert info["vertex_count"] > 64 * 65536  # the auto strategy is the frontier for clique plans here
+    plan = agpm.compile_plan(spec)
+    agpm.set_strategy(strategy)
+    try:
+        hits = [_records_equal(agpm, oracle, dg, host, info["edge_count"], plan, f, COUNT) for f in OFFSETS]
+    finally:
+        agpm.set_strategy("auto")
+    assert sum(hits) > 0
+
+
+def test_config5_class_online(agpm, oracle, rmat25):
+    dg, host, info = rmat25
+    _online_equal(agpm, oracle, dg, host, info["edge_count"], agpm.compile_plan("4clique"))
+
+
+def _host_bytes():
+    try:
+        import psutil
+
+        return psutil.virtual_memory().available
+    except Exception:
+        return 0
+
+
+@pytest.mark.skipif(_host_bytes() < (48 << 30), reason="host RAM cannot hold the oracle's RMAT-27 copy")
+def test_config5_rmat27(agpm, oracle):
+    """Config 5 itself: RMAT-27 ef16 (2.1 B edges, int64 offsets), 4-clique —
+    records at three offsets and the 1 %@95 % online stop n vs the oracle."""
+    dg, host, info = _graph(agpm, 27)
+    assert info["arcs"] > (1 << 32)  # 64-bit arc offsets are live
+    plan = agpm.compile_plan("4clique")
+    m = info["edge_count"]
+    for f in OFFSETS:
+        _records_equal(agpm, oracle, dg, host, m, plan, f, 1 << 16)
+    _online_equal(agpm, oracle, dg, host, m, plan)
