@@ -217,16 +217,22 @@ def run_gpu(args):
     import paper_2405_03488_b200 as A
 
     rank, world, local = env_rank()
-    dist = None
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    dist = comm = None
     if world > 1:
         import torch.distributed as dist
 
+        from paper_2405_03488_b200.distributed import nccl_comm
+
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     A.lib()
     A.lib().agpm_set_device(torch.cuda.current_device())
+    if dist is not None:
+        comm = nccl_comm(dist, rank, world)  # the product's NCCL communicator (moment exchange)
     dev = torch.device("cuda", torch.cuda.current_device())
     # a dedicated stream: torch's default stream has handle 0, which the C-ABI
     # reads as "the library's own stream"
@@ -249,12 +255,15 @@ def run_gpu(args):
     wins = torch.empty((nwin, 4), dtype=torch.float64, device=dev)  # 32-B accumulator records
     gathered = torch.empty((world * nwin, 4), dtype=torch.float64, device=dev) if world > 1 else None
 
+    def exchange():  # the convergence exchange: every rank's window records, rank (= id) order
+        comm.all_gather_dev(wins.data_ptr(), gathered.data_ptr(), wins.numel() * 8, sptr)
+
     def step(s):
         first = (s * world + rank) * B
         A.sample_dev(dg, plan, 1, first, B, values.data_ptr(), sptr)
         A.window_moments_dev(values.data_ptr(), B, WINDOW, wins.data_ptr(), sptr)
-        if dist is not None:
-            dist.all_gather_into_tensor(gathered, wins)
+        if comm is not None:
+            exchange()
 
     # algorithmic bytes per sample (B_min sector model), counted on device, untimed
     bmin_total = A.bmin_bytes(dg, plan, 1, 0, 1 << 22, sptr)
@@ -281,8 +290,8 @@ def run_gpu(args):
         A.sample_dev(dg, plan, 1, first, B, values.data_ptr(), sptr)
         k_end[s].record(stream)
         A.window_moments_dev(values.data_ptr(), B, WINDOW, wins.data_ptr(), sptr)
-        if dist is not None:
-            dist.all_gather_into_tensor(gathered, wins)
+        if comm is not None:
+            exchange()
     ev1.record(stream)
     torch.cuda.synchronize()
     launches = A.kernel_launches() - launches0
@@ -302,7 +311,10 @@ def run_gpu(args):
     d2h = int(((B + 4095) // 4096) * 32)
     for _ in range(2):  # untimed warm-up steps at the full budget (allocator / pinned-path first touches)
         dgh = A.DeviceGraph(g)
-        A.run_fixed_budget(dgh, plan, B, 1)
+        if comm is None:
+            A.run_fixed_budget(dgh, plan, B, 1)
+        else:
+            A.run_fixed_budget_sharded(comm, dgh, plan, B * world, 1)
         del dgh
     torch.cuda.synchronize()
     if dist is not None:
@@ -314,7 +326,10 @@ def run_gpu(args):
         t1 = time.perf_counter()
         dgh = A.DeviceGraph(g)
         t2 = time.perf_counter()
-        acc = A.run_fixed_budget(dgh, plan, B, 1 + s * world + rank)
+        if comm is None:
+            acc = A.run_fixed_budget(dgh, plan, B, 1 + s)
+        else:  # run_fixed_budget over the ranks: B ids per rank, accumulators gathered
+            acc = A.run_fixed_budget_sharded(comm, dgh, plan, B * world, 1 + s)
         t3 = time.perf_counter()
         del dgh
         up_s += t2 - t1
@@ -332,41 +347,18 @@ def run_gpu(args):
     # ---- time to converge (1%@95%) on the resident graph, rank 0's device
     ttc = None
     if world > 1:
-        # sharded run_ns_online (distributed.py): ids sharded by rank, window
-        # moments all-gathered over NCCL each batch, every rank replays the
-        # reference's window loop; wall time is the max over ranks
-        from paper_2405_03488_b200.distributed import run_ns_online_sharded
-
-        per_rank = max(WINDOW, ((1 << 19) // world // WINDOW) * WINDOW)
-        nw_b = per_rank // WINDOW
-        v_b = torch.empty(per_rank, dtype=torch.float64, device=dev)
-        w_b = torch.empty((nw_b, 4), dtype=torch.float64, device=dev)
-        g_b = torch.empty((world * nw_b, 4), dtype=torch.float64, device=dev)
-
-        def sample_moments(first, count):
-            A.sample_dev(dg, plan, 1, first, count, v_b.data_ptr(), sptr)
-            A.window_moments_dev(v_b.data_ptr(), count, WINDOW, w_b.data_ptr(), sptr)
-            torch.cuda.synchronize()
-            return w_b[: (count + WINDOW - 1) // WINDOW].cpu().numpy()
-
-        def all_gather(local):
-            w_b.copy_(torch.from_numpy(local))
-            dist.all_gather_into_tensor(g_b, w_b)
-            return g_b.cpu().numpy()
-
-        for rep in range(2):  # first run warms the path
+        # run_ns_online over the ranks (native: ids dealt per round, window records
+        # all-gathered over NCCL, every rank runs the stop test); device wall time,
+        # max over ranks
+        for rep in range(2):  # the first run warms the path
             dist.barrier()
-            torch.cuda.synchronize()
-            t_on = time.perf_counter()
-            mg = run_ns_online_sharded(sample_moments, all_gather, rank, world, 0.01, 0.05, window=WINDOW,
-                                       per_rank=per_rank)
-            torch.cuda.synchronize()
-            tt = torch.tensor([time.perf_counter() - t_on], dtype=torch.float64, device=dev)
+            mg = A.run_ns_online_sharded(comm, dg, plan, 0.01, 0.05, A.OnlinePolicy(), seed=1, stream=sptr)
+            tt = torch.tensor([mg.seconds], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         rp = mg.report
         ttc = {"seconds": float(tt.item()), "samples": rp.n, "windows": mg.windows, "estimate": rp.mu,
                "epsilon_hat": rp.epsilon_hat, "hit_rate": rp.hit_rate, "converged": bool(rp.converged),
-               "ranks": world, "samples_per_rank_per_batch": per_rank}
+               "ranks": world, "samples_launched": mg.samples_launched, "transport": "NCCL (agpm_comm)"}
     elif rank == 0:
         # cold view: a fresh device view (upload untimed), so the run includes the
         # one-time dense-core matrix and twin-arc index builds
@@ -440,8 +432,23 @@ def run_gpu(args):
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
+        comm.close()
         dist.destroy_process_group()
     return 0
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` without torchrun: re-exec under torch.distributed.run
+    with N ranks (one process per GPU) on 127.0.0.1."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -452,6 +459,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

@@ -9,19 +9,29 @@
 // behaviour mirrors the reference: std::invalid_argument, agpm::pattern_error,
 // agpm::io_error, agpm::parse_error (+ agpm::device_error for CUDA faults).
 //
-// Device mirrors of a CsrView are cached by the view's pointers: the
-// reference documents CsrGraph / CsrView as immutable (csr_graph.hpp:19-22,
-// 43-45), so pointer identity identifies the data.
+// Device mirrors of a CsrView are cached per (graph generation, GPU): every
+// CsrGraph carries a process-unique, never-reused generation id (the reference
+// documents CsrGraph / CsrView as immutable, csr_graph.hpp:19-22, 43-45), so a
+// freed graph whose addresses are recycled can never alias a new one. Views
+// built by hand (generation 0) are uploaded per call, never cached.
+//
+// `workers` / `threads` map to GPUs: with W > 1 and several visible devices,
+// min(W, devices) ranks run the sharded drivers (agpm_ns_online_sharded ...),
+// one host thread per GPU over an in-process communicator group. Results keep
+// the workers = 1 semantics of the device path (global sample id streams), so
+// they are identical for every W.
 #pragma once
 
 #include <algorithm>
 #include <cstdint>
+#include <exception>
 #include <cstring>
 #include <list>
 #include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <utility>
 #include <vector>
@@ -278,6 +288,7 @@ struct CsrView {
   const uint64_t* end = nullptr;
   const uint32_t* neighbors = nullptr;
   bool oriented = false;
+  uint64_t generation = 0;  // owner's generation id (CsrGraph::view); 0 = hand-built view
   std::span<const uint32_t> neighbors_of(uint32_t u) const { return {neighbors + begin[u], neighbors + end[u]}; }
   uint64_t degree(uint32_t u) const { return end[u] - begin[u]; }
 };
@@ -305,7 +316,9 @@ class CsrGraph {
     const uint32_t* nbr = nullptr;
     detail::check(agpm_host_graph_arrays(h_.get(), &off, &nbr));
     Info i = info();
-    return {i.n, i.m, off, off + 1, nbr, i.oriented};
+    uint64_t gen = 0;
+    detail::check(agpm_host_graph_generation(h_.get(), &gen));
+    return {i.n, i.m, off, off + 1, nbr, i.oriented, gen};
   }
   agpm_host_graph* handle() const { return h_.get(); }
 
@@ -359,51 +372,130 @@ struct OnlineResult {
 };
 
 namespace detail {
-// device mirror cache keyed by the (immutable) view's pointers
-inline agpm_graph* device_view(const CsrView& g) {
-  using Key = std::tuple<const void*, const void*, const void*, uint32_t, uint64_t, bool>;
-  struct Entry {
-    Key key;
-    agpm_graph* dev;
-  };
-  thread_local std::list<Entry> cache;
-  const Key key{g.begin, g.end, g.neighbors, g.vertex_count, g.edge_count, g.oriented};
-  for (auto it = cache.begin(); it != cache.end(); ++it)
-    if (it->key == key) {
-      cache.splice(cache.begin(), cache, it);
-      return cache.front().dev;
-    }
+using DevRef = std::shared_ptr<agpm_graph>;
+
+inline DevRef upload(const CsrView& g) {
   const bool plain = g.end == g.begin + 1;
   uint64_t len = 0;
   for (uint32_t u = 0; u < g.vertex_count; ++u) len = std::max(len, g.end[u]);
   agpm_graph* dev = nullptr;
   check(agpm_graph_upload(g.vertex_count, g.edge_count, g.begin, plain ? nullptr : g.end, g.neighbors, len,
                           g.oriented, nullptr, &dev));
-  cache.push_front({key, dev});
-  if (cache.size() > 4) {
-    agpm_graph_free(cache.back().dev);
-    cache.pop_back();
-  }
-  return dev;
+  return DevRef(dev, &agpm_graph_free);
+}
+
+// device mirror of `g` on the current GPU: cached per (generation, device) for
+// CsrGraph views (small LRU per host thread), a fresh upload for hand-built views
+inline DevRef device_view(const CsrView& g) {
+  if (g.generation == 0) return upload(g);
+  const int dev = agpm_current_device();
+  struct Entry {
+    uint64_t generation;
+    int device;
+    DevRef ref;
+  };
+  thread_local std::list<Entry> cache;
+  for (auto it = cache.begin(); it != cache.end(); ++it)
+    if (it->generation == g.generation && it->device == dev) {
+      cache.splice(cache.begin(), cache, it);
+      return cache.front().ref;
+    }
+  DevRef ref = upload(g);
+  cache.push_front({g.generation, dev, ref});
+  if (cache.size() > 8) cache.pop_back();
+  return ref;
+}
+
+// ranks for `workers`: min(workers, visible GPUs)
+inline int gpu_ranks(int workers) {
+  int n = 0;
+  check(agpm_device_count(&n));
+  return std::max(1, std::min(workers, n));
+}
+
+// run body(rank, comm, device view) on `ranks` GPUs, one host thread each; returns rank 0's value
+template <class R, class F>
+R on_ranks(const CsrView& g, int ranks, F body) {
+  agpm_comm_group* grp = nullptr;
+  check(agpm_comm_group_create(ranks, &grp));
+  std::vector<R> out(ranks);
+  std::vector<std::exception_ptr> err(ranks);
+  std::vector<std::thread> pool;
+  for (int r = 0; r < ranks; ++r)
+    pool.emplace_back([&, r] {
+      agpm_comm* c = nullptr;
+      try {
+        check(agpm_set_device(r));
+        check(agpm_comm_init_local(grp, r, &c));
+        DevRef dv = device_view(g);
+        out[r] = body(c, dv.get());
+      } catch (...) {
+        err[r] = std::current_exception();
+      }
+      if (c) agpm_comm_free(c);
+    });
+  for (auto& t : pool) t.join();
+  agpm_comm_group_free(grp);
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+  return out[0];
 }
 }  // namespace detail
 
+// SeedIndex (ns_engine.hpp:23-31, ns_engine.cpp:12-23): cumulative arc index so
+// a uniform seed arc is one bounded draw plus a binary search; plain and
+// colour-split views alike. The device path keeps its own one-gather seed-arc
+// table (csrc/device.cuh); this host index serves callers that pick arcs
+// themselves and validates the view handed to draw_sample.
+class SeedIndex {
+ public:
+  explicit SeedIndex(const CsrView& g) : prefix_(static_cast<size_t>(g.vertex_count) + 1, 0) {
+    for (uint32_t u = 0; u < g.vertex_count; ++u) prefix_[u + 1] = prefix_[u] + g.degree(u);
+  }
+  uint64_t total_arcs() const { return prefix_.back(); }
+  std::pair<uint32_t, uint32_t> arc(const CsrView& g, uint64_t index) const {
+    auto it = std::upper_bound(prefix_.begin(), prefix_.end(), index);
+    auto u = static_cast<uint32_t>((it - prefix_.begin()) - 1);
+    return {u, g.neighbors[g.begin[u] + (index - prefix_[u])]};
+  }
+
+ private:
+  std::vector<uint64_t> prefix_;
+};
+
 // draw_sample (ns_engine.cpp:92-104) for a fresh worker-0 stream CounterRng(seed, 0, id)
-inline SampledCount draw_sample(const CsrView& g, const ExecutionPlan& plan, CounterRng& rng) {
+inline SampledCount draw_sample(const CsrView& g, const SeedIndex& seeds, const ExecutionPlan& plan,
+                                CounterRng& rng) {
+  if (g.edge_count == 0) throw std::invalid_argument("cannot sample from an empty graph");
+  if (g.oriented) throw std::invalid_argument("sampling runs on the symmetric graph");
   if (!rng.fresh() || rng.stream1() != 0)
     throw std::invalid_argument("device draw_sample takes a fresh CounterRng(seed, 0, sample_id)");
+  uint64_t arcs = 0;
+  for (uint32_t u = 0; u < g.vertex_count; ++u) arcs += g.degree(u);
+  if (seeds.total_arcs() != arcs) throw std::invalid_argument("seed index was built for another view");
   double v = 0.0;
   uint8_t hit = 0;
-  detail::check(agpm_ns_draw(detail::device_view(g), &plan.c, rng.seed(), rng.stream2(), 1, &v, &hit, nullptr,
-                             nullptr));
+  detail::check(agpm_ns_draw(detail::device_view(g).get(), &plan.c, rng.seed(), rng.stream2(), 1, &v, &hit,
+                             nullptr, nullptr));
+  rng.next_u64();  // the stream is consumed, as by the reference's draw
   return {v, hit != 0, 0};
+}
+inline SampledCount draw_sample(const CsrView& g, const ExecutionPlan& plan, CounterRng& rng) {
+  return draw_sample(g, SeedIndex(g), plan, rng);
 }
 
 // run_fixed_budget (ns_engine.cpp:142-153); streams are the workers = 1 streams
 inline SampleAccumulator run_fixed_budget(const CsrView& g, const ExecutionPlan& plan, uint64_t budget,
-                                          uint64_t seed, int /*workers*/ = 1) {
+                                          uint64_t seed, int workers = 1) {
+  const int ranks = detail::gpu_ranks(workers);
+  if (ranks > 1)
+    return detail::on_ranks<SampleAccumulator>(g, ranks, [&](agpm_comm* c, agpm_graph* dv) {
+      agpm_accumulator a{};
+      detail::check(agpm_ns_fixed_budget_sharded(c, dv, &plan.c, budget, seed, &a, nullptr));
+      return detail::from_c(a);
+    });
   agpm_accumulator a{};
-  detail::check(agpm_ns_fixed_budget(detail::device_view(g), &plan.c, budget, seed, &a, nullptr));
+  detail::check(agpm_ns_fixed_budget(detail::device_view(g).get(), &plan.c, budget, seed, &a, nullptr));
   return detail::from_c(a);
 }
 
@@ -415,11 +507,21 @@ inline double hit_rate_report(const CsrView& g, const ExecutionPlan& plan, uint6
 
 // run_ns_online (ns_engine.cpp:106-140), workers = 1 window semantics
 inline OnlineResult run_ns_online(const CsrView& g, const ExecutionPlan& plan, double eps, double delta,
-                                  const OnlinePolicy& policy, uint64_t seed, int /*workers*/ = 1) {
+                                  const OnlinePolicy& policy, uint64_t seed, int workers = 1) {
   agpm_online_policy pol{policy.n_min, policy.max_samples, policy.profiled_n_samples};
+  auto wrap = [](const agpm_online_result& r) {
+    return OnlineResult{detail::from_c(r.report), detail::from_c(r.accumulator), r.windows, r.work_units};
+  };
+  const int ranks = detail::gpu_ranks(workers);
+  if (ranks > 1)
+    return detail::on_ranks<OnlineResult>(g, ranks, [&](agpm_comm* c, agpm_graph* dv) {
+      agpm_online_result r{};
+      detail::check(agpm_ns_online_sharded(c, dv, &plan.c, eps, delta, &pol, seed, &r, nullptr));
+      return wrap(r);
+    });
   agpm_online_result r{};
-  detail::check(agpm_ns_online(detail::device_view(g), &plan.c, eps, delta, &pol, seed, &r, nullptr));
-  return {detail::from_c(r.report), detail::from_c(r.accumulator), r.windows, r.work_units};
+  detail::check(agpm_ns_online(detail::device_view(g).get(), &plan.c, eps, delta, &pol, seed, &r, nullptr));
+  return wrap(r);
 }
 
 // ------------------------------------------------------------------ exact_engine.hpp
@@ -429,10 +531,37 @@ struct ExactCountResult {
 };
 
 // exact_count (exact_engine.cpp:66-91); `threads` maps to the device
-inline ExactCountResult exact_count(const CsrView& g, const ExecutionPlan& plan, int /*threads*/ = 1) {
+inline ExactCountResult exact_count(const CsrView& g, const ExecutionPlan& plan, int threads = 1) {
+  const int ranks = detail::gpu_ranks(threads);
+  if (ranks > 1)
+    return detail::on_ranks<ExactCountResult>(g, ranks, [&](agpm_comm* c, agpm_graph* dv) {
+      uint64_t n = 0;
+      detail::check(agpm_exact_count_sharded(c, dv, &plan.c, &n, nullptr));
+      return ExactCountResult{n, 0};
+    });
   uint64_t c = 0;
-  detail::check(agpm_exact_count(detail::device_view(g), &plan.c, &c, nullptr));
+  detail::check(agpm_exact_count(detail::device_view(g).get(), &plan.c, &c, nullptr));
   return {c, 0};
+}
+
+// brute_force_count (exact_engine.cpp:122-133): ground-truth oracle, <= 14 vertices
+inline uint64_t brute_force_count(const CsrGraph& g, const Pattern& pattern) {
+  const ExecutionPlan plan = compile_plan(pattern, VerifyMode::Eager);
+  const CsrView v = g.view();
+  uint64_t out = 0;
+  detail::check(agpm_brute_force_count(v.vertex_count, v.begin, v.end, v.neighbors, &plan.c, &out));
+  return out;
+}
+
+// count_matches_through_edge (exact_engine.cpp:135-213): matches whose edge set
+// contains (u, v); a work budget (candidate inspections) makes it a lower bound
+inline uint64_t count_matches_through_edge(const CsrView& g, const Pattern& pattern, uint32_t u, uint32_t v,
+                                           int64_t* work_budget = nullptr) {
+  const ExecutionPlan plan = compile_plan(pattern, VerifyMode::Eager);
+  uint64_t out = 0;
+  detail::check(agpm_count_matches_through_edge_view(g.vertex_count, g.edge_count, g.begin, g.end, g.neighbors,
+                                                     &plan.c, u, v, work_budget, &out));
+  return out;
 }
 
 // ------------------------------------------------------------------ csr_graph.hpp / gs_engine.hpp
@@ -459,7 +588,7 @@ struct GsEstimate {
 inline GsEstimate gs_estimate(const CsrGraph& g, const ExecutionPlan& plan, const SparsifyParams& params,
                               int /*threads*/ = 1) {
   agpm_gs_result r{};
-  detail::check(agpm_gs_estimate(detail::device_view(g.view()), &plan.c,
+  detail::check(agpm_gs_estimate(detail::device_view(g.view()).get(), &plan.c,
                                  params.scheme == SparsifyScheme::BernoulliEdge ? 0 : 1, params.keep_probability,
                                  params.color_count, params.seed, &r, nullptr));
   return {r.estimate, r.raw_count, r.scale, params, r.preprocess_seconds, r.search_seconds, 0};
@@ -478,6 +607,17 @@ struct KeepProbability {
   uint32_t count_ = 1;
 };
 
+// estimate_gamma (gs_engine.cpp:179-197): max matches through `probe_edges`
+// uniformly drawn arcs, a lower bound on gamma; stops once the budget is spent
+inline uint64_t estimate_gamma(const CsrView& g, const Pattern& pattern, uint64_t probe_edges, uint64_t seed,
+                               int64_t work_budget = 50000000) {
+  const ExecutionPlan plan = compile_plan(pattern, VerifyMode::Eager);
+  uint64_t out = 0;
+  detail::check(agpm_estimate_gamma_view(g.vertex_count, g.edge_count, g.begin, g.end, g.neighbors, &plan.c,
+                                         probe_edges, seed, work_budget, &out));
+  return out;
+}
+
 // choose_keep_probability (gs_engine.cpp:24-40)
 inline KeepProbability choose_keep_probability(const ReadKBoundInputs& in) {
   agpm_keep_probability k{};
@@ -494,7 +634,7 @@ class ColoredCsr {
     ColoredCsr c(g, color_count);
     c.colors_.resize(g.vertex_count());
     agpm_graph* v = nullptr;
-    detail::check(agpm_color_split(detail::device_view(g.view()), color_count, seed, c.colors_.data(), &c.same_,
+    detail::check(agpm_color_split(detail::device_view(g.view()).get(), color_count, seed, c.colors_.data(), &c.same_,
                                    &v, nullptr));
     c.view_.reset(v, &agpm_graph_free);
     return c;
@@ -503,7 +643,7 @@ class ColoredCsr {
     ColoredCsr c(g, color_count);
     c.colors_ = std::move(colors);
     agpm_graph* v = nullptr;
-    detail::check(agpm_color_split_with_colors(detail::device_view(g.view()), c.colors_.data(), color_count,
+    detail::check(agpm_color_split_with_colors(detail::device_view(g.view()).get(), c.colors_.data(), color_count,
                                                &c.same_, &v, nullptr));
     c.view_.reset(v, &agpm_graph_free);
     return c;
@@ -515,7 +655,7 @@ class ColoredCsr {
     ColoredCsr c(base_, coarse_count);
     c.colors_.resize(base_.vertex_count());
     agpm_graph* v = nullptr;
-    detail::check(agpm_merge_colors(detail::device_view(base_.view()), colors_.data(), color_count_,
+    detail::check(agpm_merge_colors(detail::device_view(base_.view()).get(), colors_.data(), color_count_,
                                     group_map.data(), static_cast<uint32_t>(group_map.size()), c.colors_.data(),
                                     &c.same_, &v, nullptr));
     c.view_.reset(v, &agpm_graph_free);
@@ -587,7 +727,7 @@ inline ProfileResult fast_profile(const CsrGraph& g, const ExecutionPlan& plan, 
                                   double user_epsilon, uint64_t seed, int /*threads*/ = 1,
                                   uint64_t profiler_sample_cap = 1000000) {
   agpm_profile_result r{};
-  detail::check(agpm_fast_profile(detail::device_view(g.view()), &plan.c, profile_fraction, user_epsilon, seed,
+  detail::check(agpm_fast_profile(detail::device_view(g.view()).get(), &plan.c, profile_fraction, user_epsilon, seed,
                                   profiler_sample_cap, &r, nullptr));
   return {r.n_samples_estimate, r.mu_prime, r.scaled_count, r.epsilon_hat_final, r.n_converged, r.fraction,
           r.reliable != 0, r.seconds};

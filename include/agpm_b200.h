@@ -11,7 +11,8 @@
  * (reference = /root/reference/proj, "agpm" C++20 library).
  *
  * Stream semantics: every call that takes `void* stream` accepts a
- * cudaStream_t (NULL = the library's own non-blocking per-device stream; pass
+ * cudaStream_t (NULL = the library's own non-blocking stream for the calling
+ * host thread and current device; pass
  * cudaStreamLegacy, (void*)1, for the legacy default stream). Calls that return
  * host results synchronise that stream before returning; *_dev calls only
  * enqueue work.
@@ -121,6 +122,8 @@ int agpm_host_graph_info(const agpm_host_graph* g, uint32_t* n, uint64_t* edge_c
 int agpm_host_graph_arrays(const agpm_host_graph* g, const uint64_t** offsets,
                            const uint32_t** neighbors);
 void agpm_host_graph_free(agpm_host_graph* g);
+/* process-unique, never-reused id of a host graph (keys device-mirror caches) */
+int agpm_host_graph_generation(const agpm_host_graph* g, uint64_t* out);
 
 /* Relabel so vertex id = rank of (degree, id): the reference's id-order
  * symmetry constraints then coincide with degree orientation. */
@@ -349,6 +352,18 @@ int agpm_count_matches_through_edge(const agpm_host_graph* g, const agpm_plan* p
                                     uint64_t* out);
 int agpm_estimate_gamma(const agpm_host_graph* g, const agpm_plan* plan, uint64_t probe_edges, uint64_t seed,
                         int64_t work_budget, uint64_t* out);
+/* brute_force_count (exact_engine.cpp:93-133): injective maps honouring the
+ * induced mode / |Aut|, independent of the plan machinery; small graphs */
+int agpm_brute_force_count(uint32_t n, const uint64_t* begin, const uint64_t* end, const uint32_t* neighbors,
+                           const agpm_plan* plan, uint64_t* out);
+/* the same two on a host CsrView (begin/end per vertex; end NULL = plain), with the
+ * reference's optional in/out work budget (exact_engine.hpp:29-33, gs_engine.hpp:56-60) */
+int agpm_count_matches_through_edge_view(uint32_t n, uint64_t edge_count, const uint64_t* begin,
+                                         const uint64_t* end, const uint32_t* neighbors, const agpm_plan* plan,
+                                         uint32_t u, uint32_t v, int64_t* work_budget, uint64_t* out);
+int agpm_estimate_gamma_view(uint32_t n, uint64_t edge_count, const uint64_t* begin, const uint64_t* end,
+                             const uint32_t* neighbors, const agpm_plan* plan, uint64_t probe_edges, uint64_t seed,
+                             int64_t work_budget, uint64_t* out);
 int agpm_fast_profile(agpm_graph* g, const agpm_plan* plan, double profile_fraction, double user_epsilon,
                       uint64_t seed, uint64_t profiler_sample_cap, agpm_profile_result* out, void* stream);
 /* device analogue of calibrate_hardware_constant (cost_model.cpp:31-76): seconds
@@ -392,10 +407,68 @@ int agpm_region_split(agpm_graph* g, const agpm_plan* plan, uint32_t tau_degree,
                       double delta, uint64_t seed, uint32_t colors, uint32_t repeats, uint64_t max_samples,
                       agpm_region_result* out, void* stream);
 
+/* ------------------------------------------------------- multi-GPU -------
+ * SURVEY §8(e). The reference fans a window out over `workers` threads and
+ * merges their accumulators in worker order (ns_engine.cpp:64-88, 121-137);
+ * here a rank is one GPU holding a full replica of the view, global sample ids
+ * are dealt to ranks in per-batch blocks (batch b, rank r: ids
+ * [L_b + r*B, L_b + (r+1)*B)), each rank folds its block into window moments,
+ * and the 32-B window records are all-gathered — rank order is id order, so
+ * every rank runs the single-GPU stop test (converge_kernel) on the same
+ * records and reaches the same decision: stop n, hits and sums equal the
+ * single-GPU (= reference workers=1) run for every rank count.
+ *
+ * Communicators: NCCL (one process per GPU; rank 0 calls agpm_nccl_unique_id
+ * and the caller broadcasts the 128 bytes), or a local group of `world` ranks
+ * driven by host threads of one process (one thread per GPU; several ranks may
+ * share a GPU — exchanges are host-synchronised peer copies, no kernel waits on
+ * another rank). Create the communicator on the rank's device (cudaSetDevice
+ * or agpm_set_device first). */
+#define AGPM_NCCL_ID_BYTES 128
+typedef struct agpm_comm agpm_comm;
+typedef struct agpm_comm_group agpm_comm_group;
+int agpm_nccl_unique_id(unsigned char id[AGPM_NCCL_ID_BYTES]);
+int agpm_comm_init_nccl(int rank, int world, const unsigned char id[AGPM_NCCL_ID_BYTES], agpm_comm** out);
+int agpm_comm_group_create(int world, agpm_comm_group** out);
+int agpm_comm_init_local(agpm_comm_group* group, int rank, agpm_comm** out);
+int agpm_comm_group_free(agpm_comm_group* group); /* after every member's agpm_comm_free */
+int agpm_comm_free(agpm_comm* c);
+int agpm_comm_info(const agpm_comm* c, int* rank, int* world, int* device, int* is_nccl);
+/* enqueue an all-gather of device buffers on `stream`: d_recv[r*bytes ..] = rank r's d_send
+ * (the exchange step of the sharded drivers, exposed for callers that drive
+ * agpm_ns_sample_dev / agpm_window_moments_dev themselves) */
+int agpm_comm_all_gather_dev(agpm_comm* c, const void* d_send, void* d_recv, uint64_t bytes_per_rank, void* stream);
+/* run_ns_online (ns_engine.cpp:106-140) over the ranks of `c`; every rank
+ * passes its own replica `g` and receives the same result (samples_launched
+ * and seconds are global / this rank's). */
+int agpm_ns_online_sharded(agpm_comm* c, agpm_graph* g, const agpm_plan* plan, double eps, double delta,
+                           const agpm_online_policy* policy, uint64_t seed, agpm_online_result* out,
+                           void* stream);
+/* The id partition agpm_ns_online_sharded uses (host arithmetic, no device):
+ * round of `launched` ids so far, per-rank block `batch` (a multiple of
+ * `window`) -> this rank's first id / count, the round's id count, the number
+ * of valid (id-ordered, prefix) window records in the gather and the records
+ * each rank contributes. Exposed so multi-rank host logic can be tested on CPU. */
+typedef struct agpm_shard_round {
+  uint64_t first_id, count, round_ids, valid_windows, windows_per_rank;
+} agpm_shard_round;
+int agpm_ns_shard_round(uint64_t launched, uint64_t batch, uint64_t window, uint64_t max_samples, int rank,
+                        int world, agpm_shard_round* out);
+/* run_fixed_budget (ns_engine.cpp:142-153) over the ranks: rank r draws the
+ * r-th contiguous share of ids [0, budget); accumulators gathered and folded in
+ * rank order (n, hits exact; sums equal up to reduction-order rounding). */
+int agpm_ns_fixed_budget_sharded(agpm_comm* c, agpm_graph* g, const agpm_plan* plan, uint64_t budget,
+                                 uint64_t seed, agpm_accumulator* out, void* stream);
+/* exact_count (exact_engine.cpp:66-91) over the ranks (agpm_exact_count_shard
+ * per rank, u64 partials summed) */
+int agpm_exact_count_sharded(agpm_comm* c, agpm_graph* g, const agpm_plan* plan, uint64_t* count, void* stream);
+
 /* ------------------------------------------------------- misc / device -----*/
 const char* agpm_last_error(void);
 int agpm_device_count(int* n);
 int agpm_set_device(int device);
+/* the calling thread's current CUDA device (-1 if none) */
+int agpm_current_device(void);
 int agpm_version(void);
 int agpm_sync(void* stream);
 /* kernels launched by this library since load (evidence for the bench) */

@@ -29,6 +29,8 @@ __all__ = [
     "hit_rate_report", "exact_count", "exact_count_rooted", "region_split", "gs_estimate", "choose_keep_probability", "ns_cost_cone",
     "gs_cost_estimate", "select_scheme", "count_matches_through_edge", "estimate_gamma", "fast_profile",
     "calibrate_hardware_constant", "count_hybrid", "exact_count_shard", "gs_online", "bmin_bytes", "set_strategy", "set_rng", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "Comm", "LocalGroup", "nccl_unique_id", "shard_round", "run_ns_online_sharded", "run_fixed_budget_sharded",
+    "exact_count_sharded",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
 ]
 
@@ -159,6 +161,20 @@ def _declare(L):
         "agpm_ns_set_frontier_reuse": (C.c_int, [C.c_int]),
         "agpm_ns_set_core_dim": (C.c_int, [A.u32]),
         "agpm_ns_set_rng": (C.c_int, [C.c_int]),
+        "agpm_nccl_unique_id": (C.c_int, [C.c_char_p]),
+        "agpm_comm_init_nccl": (C.c_int, [C.c_int, C.c_int, C.c_char_p, C.POINTER(A.P)]),
+        "agpm_comm_group_create": (C.c_int, [C.c_int, C.POINTER(A.P)]),
+        "agpm_comm_init_local": (C.c_int, [A.P, C.c_int, C.POINTER(A.P)]),
+        "agpm_comm_group_free": (C.c_int, [A.P]),
+        "agpm_comm_free": (C.c_int, [A.P]),
+        "agpm_comm_info": (C.c_int, [A.P] + [C.POINTER(C.c_int)] * 4),
+        "agpm_ns_shard_round": (C.c_int, [A.u64, A.u64, A.u64, A.u64, C.c_int, C.c_int,
+                                          C.POINTER(A.ShardRound)]),
+        "agpm_ns_online_sharded": (C.c_int, [A.P, A.P, A.pPlan, C.c_double, C.c_double, C.POINTER(OnlinePolicy),
+                                             A.u64, C.POINTER(OnlineResult), A.P]),
+        "agpm_ns_fixed_budget_sharded": (C.c_int, [A.P, A.P, A.pPlan, A.u64, A.u64, A.pAcc, A.P]),
+        "agpm_exact_count_sharded": (C.c_int, [A.P, A.P, A.pPlan, A.pu64, A.P]),
+        "agpm_comm_all_gather_dev": (C.c_int, [A.P, A.P, A.P, A.u64, A.P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -649,6 +665,100 @@ def set_rng(policy):
 def set_frontier_reuse(on):
     """Frontier sampler: reuse nested survivors between clique steps (same samples)."""
     _check(lib().agpm_ns_set_frontier_reuse(int(bool(on))))
+
+
+# ------------------------------------------------------------------ multi-GPU (SURVEY §8(e))
+class Comm:
+    """A rank communicator (agpm_comm): NCCL (one process per GPU) or a member
+    of a LocalGroup (host threads of one process). Create it on the rank's GPU."""
+
+    def __init__(self, handle, group=None):
+        self._h = handle
+        self._group = group  # keeps the group alive while a member exists
+
+    @classmethod
+    def nccl(cls, rank, world, unique_id):
+        h = C.c_void_p()
+        _check(lib().agpm_comm_init_nccl(rank, world, bytes(unique_id), C.byref(h)))
+        return cls(h)
+
+    def info(self):
+        r, w, d, n = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(lib().agpm_comm_info(self._h, C.byref(r), C.byref(w), C.byref(d), C.byref(n)))
+        return {"rank": r.value, "world": w.value, "device": d.value, "nccl": bool(n.value)}
+
+    def all_gather_dev(self, d_send_ptr, d_recv_ptr, bytes_per_rank, stream=None):
+        """Enqueue recv[r * bytes ...] = rank r's send (device pointers) on `stream`."""
+        _check(lib().agpm_comm_all_gather_dev(self._h, C.c_void_p(d_send_ptr), C.c_void_p(d_recv_ptr),
+                                              bytes_per_rank, None if stream is None else C.c_void_p(stream)))
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h and h.value and _lib is not None:
+            _lib.agpm_comm_free(h)
+            self._h = None
+        self._group = None
+
+    def __del__(self):
+        self.close()
+
+
+class LocalGroup:
+    """`world` ranks driven by host threads of this process (agpm_comm_group)."""
+
+    def __init__(self, world):
+        h = C.c_void_p()
+        _check(lib().agpm_comm_group_create(world, C.byref(h)))
+        self._h = h
+        self.world = world
+
+    def comm(self, rank):
+        """The communicator of `rank`; call from the thread (and device) that drives it."""
+        h = C.c_void_p()
+        _check(lib().agpm_comm_init_local(self._h, rank, C.byref(h)))
+        return Comm(h, self)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value and _lib is not None:
+            _lib.agpm_comm_group_free(h)
+            self._h = None
+
+
+def nccl_unique_id():
+    """ncclGetUniqueId (128 bytes): rank 0 makes it, the caller broadcasts it."""
+    buf = C.create_string_buffer(_abi.NCCL_ID_BYTES)
+    _check(lib().agpm_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_round(launched, batch, window, max_samples, rank, world):
+    """The id partition of one round of run_ns_online_sharded (host arithmetic)."""
+    out = _abi.ShardRound()
+    _check(lib().agpm_ns_shard_round(launched, batch, window, max_samples, rank, world, C.byref(out)))
+    return out
+
+
+def run_ns_online_sharded(comm, dg, plan, eps, delta, policy=None, seed=1, stream=None):
+    """run_ns_online (ns_engine.cpp:106-140) over the ranks of `comm`: every rank
+    passes its replica and gets the single-GPU (= reference workers=1) result."""
+    res = OnlineResult()
+    pol = policy if policy is not None else OnlinePolicy()
+    _check(lib().agpm_ns_online_sharded(comm._h, dg._h, C.byref(plan), eps, delta, C.byref(pol), seed,
+                                        C.byref(res), stream))
+    return res
+
+
+def run_fixed_budget_sharded(comm, dg, plan, budget, seed, stream=None):
+    acc = Accumulator()
+    _check(lib().agpm_ns_fixed_budget_sharded(comm._h, dg._h, C.byref(plan), budget, seed, C.byref(acc), stream))
+    return acc
+
+
+def exact_count_sharded(comm, dg, plan, stream=None):
+    out = C.c_uint64()
+    _check(lib().agpm_exact_count_sharded(comm._h, dg._h, C.byref(plan), C.byref(out), stream))
+    return out.value
 
 
 def kernel_launches():

@@ -154,3 +154,12 @@ P = C.c_void_p
 u32, u64, i32, dbl = C.c_uint32, C.c_uint64, C.c_int, C.c_double
 pu32, pu64, pdbl, pu8 = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_uint8)
 pPlan, pAcc = C.POINTER(Plan), C.POINTER(Accumulator)
+
+
+class ShardRound(C.Structure):
+    """agpm_shard_round: this rank's ids in one round of the sharded online loop."""
+    _fields_ = [("first_id", C.c_uint64), ("count", C.c_uint64), ("round_ids", C.c_uint64),
+                ("valid_windows", C.c_uint64), ("windows_per_rank", C.c_uint64)]
+
+
+NCCL_ID_BYTES = 128

@@ -1,4 +1,5 @@
 // C-ABI for host CSR graphs and generators (include/agpm_b200.h).
+#include <atomic>
 #include <cstring>
 
 #include "common.hpp"
@@ -17,7 +18,20 @@ void need(const void* p) {
 }
 }  // namespace
 
+uint64_t agpm_b200_next_generation() {
+  static std::atomic<uint64_t> next{1};
+  return next.fetch_add(1);
+}
+
 extern "C" {
+
+int agpm_host_graph_generation(const agpm_host_graph* g, uint64_t* out) {
+  return guarded([&] {
+    need(g);
+    need(out);
+    *out = g->generation;
+  });
+}
 
 int agpm_host_graph_from_edges(const uint32_t* edges, uint64_t n_edges, uint32_t min_n,
                                agpm_host_graph** out) {

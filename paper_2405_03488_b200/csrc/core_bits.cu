@@ -82,24 +82,44 @@ __global__ void twin_kernel(const VtxInfo* __restrict__ vtx, const uint32_t* __r
 
 }  // namespace
 
+// The twin index is a speed hint (identical samples without it): it is built
+// best-effort — skipped when HBM is short (4 B per arc, 16.9 GB on RMAT-27) —
+// and published only once its build kernel has finished, under the view's
+// index lock, so no launch on any stream or host thread can see a pointer to
+// an index still being written.
 void ensure_twin_arcs(agpm_graph* g, cudaStream_t s) {
   if (g->twin || !g->plain || g->oriented || g->arcs == 0) return;
+  std::lock_guard<std::mutex> lk(g->index_mu);
+  if (g->twin) return;
+  const size_t need = 4ull * g->arcs;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || free_b < need + (2ull << 30)) {
+    cudaGetLastError();
+    return;
+  }
   uint32_t* tw = nullptr;
-  AGPM_CUDA(dev_malloc(&tw, 4ull * g->arcs));
+  if (dev_malloc(&tw, need) != cudaSuccess) {
+    cudaGetLastError();  // out of memory: sample without the hint
+    return;
+  }
   DeviceCtx& ctx = ctx_for_current_device();
   const unsigned blocks = (unsigned)std::min<unsigned long long>((g->arcs + 255) / 256, (unsigned long long)ctx.sm_count * 16);
   twin_kernel<<<blocks, 256, 0, s>>>(g->vtx, g->nbr, g->seed_arcs, g->arcs, tw);
   count_launch();
   AGPM_CUDA(cudaGetLastError());
+  AGPM_CUDA(cudaStreamSynchronize(s));
+  g->bytes += need;
   g->twin = tw;
-  g->bytes += 4ull * g->arcs;
 }
 
 void set_core_dim(uint32_t dim) { g_core_dim = dim; }
 uint32_t core_dim_setting() { return g_core_dim; }
 
+// Published after its build finished, under the view's index lock (see ensure_twin_arcs).
 void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
   const uint32_t want = g->oriented || !g->plain ? 0u : std::min(g_core_dim, g->n);
+  if (g->core && g->core_dim == want) return;
+  std::lock_guard<std::mutex> lk(g->index_mu);
   if (g->core && g->core_dim == want) return;
   if (g->core) {
     AGPM_CUDA(cudaStreamSynchronize(s));
@@ -121,6 +141,7 @@ void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
   core_rows_kernel<<<blocks, 256, shmem, s>>>(g->vtx, g->nbr, base, want, wpr, bits);
   count_launch();
   AGPM_CUDA(cudaGetLastError());
+  AGPM_CUDA(cudaStreamSynchronize(s));
   g->core = bits;
   g->core_base = base;
   g->core_wpr = wpr;

@@ -60,15 +60,30 @@ bool sorted_contains(const uint32_t* s, uint64_t len, uint32_t x) {
 
 }  // namespace
 
-// count_matches_through_edge (exact_engine.cpp:135-213) on a host CSR
-uint64_t count_matches_through_edge_host(const HostGraph& g, const agpm_plan& p, uint32_t u, uint32_t v,
+// A host CsrView (csr_graph.hpp:23-41): begin/end per vertex, so split views work too.
+struct HostView {
+  uint32_t n = 0;
+  uint64_t edge_count = 0;
+  const uint64_t* begin = nullptr;
+  const uint64_t* end = nullptr;
+  const uint32_t* nbr = nullptr;
+  uint64_t degree(uint32_t x) const { return end[x] - begin[x]; }
+};
+
+HostView view_of(const HostGraph& g) {
+  return {g.n, g.edge_count, g.offsets.data(), g.offsets.data() + 1, g.neighbors.data()};
+}
+
+// count_matches_through_edge (exact_engine.cpp:135-213) on a host view
+uint64_t count_matches_through_edge_view(const HostView& g, const agpm_plan& p, uint32_t u, uint32_t v,
                                          int64_t* work_budget) {
+  if (u >= g.n || v >= g.n) throw std::invalid_argument("edge endpoint out of range");
   const int k = p.k;
   uint64_t maps = 0;
   std::vector<uint32_t> image(k, 0);
   std::vector<bool> used(g.n, false);
   std::vector<int> ext_order;
-  auto nb = [&](uint32_t x) { return g.neighbors.data() + g.offsets[x]; };
+  auto nb = [&](uint32_t x) { return g.nbr + g.begin[x]; };
   std::function<uint64_t(size_t, uint32_t)> extend = [&](size_t depth, uint32_t assigned) -> uint64_t {
     if (depth == ext_order.size()) return 1;
     if (work_budget && *work_budget <= 0) return 0;
@@ -129,21 +144,33 @@ uint64_t count_matches_through_edge_host(const HostGraph& g, const agpm_plan& p,
   return maps / automorphism_count(p);
 }
 
+uint64_t count_matches_through_edge_host(const HostGraph& g, const agpm_plan& p, uint32_t u, uint32_t v,
+                                         int64_t* work_budget) {
+  return count_matches_through_edge_view(view_of(g), p, u, v, work_budget);
+}
+
 // estimate_gamma (gs_engine.cpp:179-197)
-uint64_t estimate_gamma_host(const HostGraph& g, const agpm_plan& p, uint64_t probe_edges, uint64_t seed,
+uint64_t estimate_gamma_view(const HostView& g, const agpm_plan& p, uint64_t probe_edges, uint64_t seed,
                              int64_t work_budget) {
   if (probe_edges < 1) throw std::invalid_argument("probe count must be >= 1");
   if (g.edge_count == 0) return 0;
+  std::vector<uint64_t> prefix(static_cast<size_t>(g.n) + 1, 0);
+  for (uint32_t x = 0; x < g.n; ++x) prefix[x + 1] = prefix[x] + g.degree(x);
   CounterRng rng(seed, 0x67616d6dull);  // "gamm"
   uint64_t best = 0;
   for (uint64_t i = 0; i < probe_edges && work_budget > 0; ++i) {
-    const uint64_t idx = rng.next_below(g.offsets.back());
-    const auto it = std::upper_bound(g.offsets.begin(), g.offsets.end(), idx);
-    const auto u = static_cast<uint32_t>((it - g.offsets.begin()) - 1);
-    const uint32_t v = g.neighbors[idx];
-    best = std::max(best, count_matches_through_edge_host(g, p, u, v, &work_budget));
+    const uint64_t idx = rng.next_below(prefix.back());
+    const auto it = std::upper_bound(prefix.begin(), prefix.end(), idx);
+    const auto u = static_cast<uint32_t>((it - prefix.begin()) - 1);
+    const uint32_t v = g.nbr[g.begin[u] + (idx - prefix[u])];
+    best = std::max(best, count_matches_through_edge_view(g, p, u, v, &work_budget));
   }
   return best;
+}
+
+uint64_t estimate_gamma_host(const HostGraph& g, const agpm_plan& p, uint64_t probe_edges, uint64_t seed,
+                             int64_t work_budget) {
+  return estimate_gamma_view(view_of(g), p, probe_edges, seed, work_budget);
 }
 
 }  // namespace agpm_b200
@@ -223,6 +250,62 @@ int agpm_count_matches_through_edge(const agpm_host_graph* g, const agpm_plan* p
 int agpm_estimate_gamma(const agpm_host_graph* g, const agpm_plan* plan, uint64_t probe_edges, uint64_t seed,
                         int64_t work_budget, uint64_t* out) {
   return guarded([&] { *out = estimate_gamma_host(g->g, *plan, probe_edges, seed, work_budget); });
+}
+
+int agpm_brute_force_count(uint32_t n, const uint64_t* begin, const uint64_t* end, const uint32_t* neighbors,
+                           const agpm_plan* plan, uint64_t* out) {
+  // exact_engine.cpp:93-133: every injective map of the pattern (vertex order
+  // 0..k-1) into the graph whose mapped pattern edges are graph edges (and, in
+  // the induced mode, whose non-edges are not), divided by |Aut|
+  return guarded([&] {
+    if (!begin || !plan || !out || (n && !neighbors)) throw std::invalid_argument("null argument");
+    if (n > 14) throw std::invalid_argument("brute-force oracle is limited to 14 vertices");
+    const HostView g{n, 0, begin, end ? end : begin + 1, neighbors};
+    const agpm_plan& p = *plan;
+    std::vector<uint32_t> image(p.k, 0);
+    std::vector<bool> used(n, false);
+    auto adjacent = [&](uint32_t a, uint32_t b) { return sorted_contains(g.nbr + g.begin[a], g.degree(a), b); };
+    std::function<uint64_t(int)> place = [&](int pv) -> uint64_t {
+      if (pv == p.k) return 1;
+      uint64_t total = 0;
+      for (uint32_t x = 0; x < n; ++x) {
+        if (used[x]) continue;
+        bool ok = true;
+        for (int q = 0; q < pv && ok; ++q) {
+          const bool want = has_edge(p, q, pv);
+          if (!want && !p.induced) continue;
+          if (want != adjacent(image[q], x)) ok = false;
+        }
+        if (!ok) continue;
+        image[pv] = x;
+        used[x] = true;
+        total += place(pv + 1);
+        used[x] = false;
+      }
+      return total;
+    };
+    *out = place(0) / automorphism_count(p);
+  });
+}
+
+int agpm_count_matches_through_edge_view(uint32_t n, uint64_t edge_count, const uint64_t* begin,
+                                         const uint64_t* end, const uint32_t* neighbors, const agpm_plan* plan,
+                                         uint32_t u, uint32_t v, int64_t* work_budget, uint64_t* out) {
+  return guarded([&] {
+    if (!begin || !plan || !out || (n && !neighbors)) throw std::invalid_argument("null argument");
+    const HostView g{n, edge_count, begin, end ? end : begin + 1, neighbors};
+    *out = count_matches_through_edge_view(g, *plan, u, v, work_budget);
+  });
+}
+
+int agpm_estimate_gamma_view(uint32_t n, uint64_t edge_count, const uint64_t* begin, const uint64_t* end,
+                             const uint32_t* neighbors, const agpm_plan* plan, uint64_t probe_edges, uint64_t seed,
+                             int64_t work_budget, uint64_t* out) {
+  return guarded([&] {
+    if (!begin || !plan || !out || (n && !neighbors)) throw std::invalid_argument("null argument");
+    const HostView g{n, edge_count, begin, end ? end : begin + 1, neighbors};
+    *out = estimate_gamma_view(g, *plan, probe_edges, seed, work_budget);
+  });
 }
 
 int agpm_fast_profile(agpm_graph* g, const agpm_plan* plan, double profile_fraction, double user_epsilon,

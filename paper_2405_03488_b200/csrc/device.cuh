@@ -12,7 +12,9 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <string>
 
 #include "agpm_b200.h"
@@ -63,6 +65,24 @@ cudaError_t dev_malloc(T** p, size_t bytes) {
 cudaStream_t pick_stream(void* stream);
 void count_launch(uint64_t n = 1);
 
+// Makes `device` current for a scope (every call on a graph runs on the GPU
+// that holds it, whatever device the calling thread had selected).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != device) {
+      cuda_check(cudaSetDevice(device), "cudaSetDevice");
+      prev = cur;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 }  // namespace agpm_b200
 
 // C-ABI opaque handle
@@ -78,12 +98,11 @@ struct agpm_graph {
   agpm_b200::VtxInfo* vtx = nullptr;
   uint32_t* nbr = nullptr;
   unsigned long long* seed_arcs = nullptr;
-  unsigned long long* ehash = nullptr;  // edge-membership table (edge_hash.cuh), built on demand
-  uint32_t ehash_mask = 0;
   uint32_t* core = nullptr;  // dense-core bit matrix (core_bits.cu), built on demand
   uint32_t core_base = 0, core_wpr = 0, core_dim = 0;
   uint32_t* twin = nullptr;  // twin[i] = position of u in N(v) for arc i = (u -> v); plain views, on demand
-  uint32_t sample_calls = 0;  // sampling launches on this view (the twin index is built on reuse)
+  std::atomic<uint32_t> sample_calls{0};  // sampling launches on this view (the twin index is built on reuse)
+  std::mutex index_mu;  // serialises the lazy index builds (core bits, twin arcs) of this view
   uint64_t bytes = 0;
 };
 
@@ -93,8 +112,6 @@ namespace agpm_b200 {
 // ownership of nothing; g->nbr must be set.
 void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsigned long long* d_end,
                    cudaStream_t s);
-// build g->ehash if absent (symmetric or oriented views alike: keys are unordered pairs)
-void ensure_edge_hash(agpm_graph* g, cudaStream_t s);
 // build (or drop, when the configured dimension is 0) g->core for the current core dimension
 void ensure_core_bits(agpm_graph* g, cudaStream_t s);
 uint32_t core_dim_setting();

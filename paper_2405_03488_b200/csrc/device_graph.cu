@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <sys/syscall.h>
+#include <unistd.h>
 #include <vector>
 
 #include "device.cuh"
@@ -18,7 +20,7 @@ namespace {
 thread_local std::string t_err;
 std::atomic<uint64_t> g_launches{0};
 std::mutex g_ctx_mu;
-DeviceCtx* g_ctx[64] = {nullptr};
+bool g_pool_ready[64] = {false};
 }  // namespace
 
 void set_last_error(const std::string& msg) { t_err = msg; }
@@ -35,7 +37,7 @@ struct Parked {
 };
 std::mutex g_park_mu;
 std::vector<Parked> g_parked;
-std::unordered_map<void*, size_t> g_big;  // live large blocks -> size
+std::unordered_map<void*, std::pair<size_t, int>> g_big;  // live large blocks -> (size, owning device)
 size_t g_parked_bytes = 0;
 constexpr size_t kParkMin = 32ull << 20, kParkMax = 1ull << 30, kParkCap = 4ull << 30;
 }  // namespace
@@ -49,7 +51,7 @@ cudaError_t dev_malloc_bytes(void** p, size_t bytes) {
         *p = g_parked[i].p;
         g_parked_bytes -= bytes;
         g_parked.erase(g_parked.begin() + (long)i);
-        g_big[*p] = bytes;
+        g_big[*p] = {bytes, ctx.device};
         return cudaSuccess;
       }
   }
@@ -58,7 +60,7 @@ cudaError_t dev_malloc_bytes(void** p, size_t bytes) {
   e = cudaStreamSynchronize(ctx.stream);
   if (e == cudaSuccess && bytes >= kParkMin && bytes <= kParkMax) {
     std::lock_guard<std::mutex> lk(g_park_mu);
-    g_big[*p] = bytes;
+    g_big[*p] = {bytes, ctx.device};
   }
   return e;
 }
@@ -72,10 +74,11 @@ cudaError_t dev_free(void* p) {
     std::lock_guard<std::mutex> lk(g_park_mu);
     auto it = g_big.find(p);
     if (it != g_big.end()) {
-      const size_t bytes = it->second;
+      const size_t bytes = it->second.first;
+      const int owner = it->second.second;  // parked under the GPU that holds it
       g_big.erase(it);
       if (g_parked_bytes + bytes <= kParkCap) {  // idle (device synchronised above): reusable at once
-        g_parked.push_back({p, bytes, ctx.device});
+        g_parked.push_back({p, bytes, owner});
         g_parked_bytes += bytes;
         return cudaSuccess;
       }
@@ -120,6 +123,33 @@ void* DeviceCtx::get_pinned(int slot, size_t bytes) {
   return pinned[slot];
 }
 
+// One context (stream + scratch) per host thread and device: host threads
+// driving ranks of a local group — several may share a GPU — never share
+// scratch buffers or the library stream. A worker thread's contexts are
+// released when it exits; the main thread's live until process exit.
+namespace {
+struct ThreadCtxs {
+  DeviceCtx* c[64] = {nullptr};
+  ~ThreadCtxs() {
+    if (static_cast<pid_t>(syscall(SYS_gettid)) == getpid()) return;  // main thread: process teardown
+    for (int d = 0; d < 64; ++d) {
+      DeviceCtx* x = c[d];
+      if (!x) continue;
+      if (cudaSetDevice(d) == cudaSuccess) {
+        cudaStreamSynchronize(x->stream);
+        for (void* p : x->scratch)
+          if (p) dev_free(p);
+        for (void* p : x->pinned)
+          if (p) cudaFreeHost(p);
+        cudaStreamDestroy(x->stream);
+      }
+      delete x;
+    }
+  }
+};
+thread_local ThreadCtxs t_ctx;
+}  // namespace
+
 DeviceCtx& ctx_for_current_device() {
   int dev = 0;
   int count = 0;
@@ -127,19 +157,24 @@ DeviceCtx& ctx_for_current_device() {
   if (e != cudaSuccess || count == 0)
     throw nodevice_error("no CUDA device visible: the B200 sampling path has no CPU fallback");
   AGPM_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lk(g_ctx_mu);
-  if (!g_ctx[dev]) {
+  if (!t_ctx.c[dev]) {
     auto* c = new DeviceCtx();
     c->device = dev;
     AGPM_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev));
     AGPM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    cudaMemPool_t pool;
-    AGPM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t keep = ~0ull;  // never trim: freed graph memory stays cached for the next view
-    AGPM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    g_ctx[dev] = c;
+    {
+      std::lock_guard<std::mutex> lk(g_ctx_mu);
+      if (!g_pool_ready[dev]) {
+        cudaMemPool_t pool;
+        AGPM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = ~0ull;  // never trim: freed graph memory stays cached for the next view
+        AGPM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        g_pool_ready[dev] = true;
+      }
+    }
+    t_ctx.c[dev] = c;
   }
-  return *g_ctx[dev];
+  return *t_ctx.c[dev];
 }
 
 cudaStream_t pick_stream(void* stream) {
@@ -259,6 +294,15 @@ int agpm_set_device(int device) {
   return guarded([&] { AGPM_CUDA(cudaSetDevice(device)); });
 }
 
+int agpm_current_device(void) {
+  int d = -1;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return d;
+}
+
 int agpm_sync(void* stream) {
   return guarded([&] { AGPM_CUDA(cudaStreamSynchronize(pick_stream(stream))); });
 }
@@ -299,10 +343,10 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
 int agpm_graph_free(agpm_graph* g) {
   return guarded([&] {
     if (!g) return;
+    DeviceGuard guard(g->device);  // free (and park) on the GPU that holds the view
     dev_free(g->vtx);
     dev_free(g->nbr);
     dev_free(g->seed_arcs);
-    if (g->ehash) dev_free(g->ehash);
     if (g->core) dev_free(g->core);
     if (g->twin) dev_free(g->twin);
     delete g;

@@ -3,7 +3,6 @@
 // (fused: ns_frontier.cu, flat: ns_flat.cu).
 #pragma once
 
-#include "edge_hash.cuh"
 #include "ns_common.cuh"
 
 namespace agpm_b200 {

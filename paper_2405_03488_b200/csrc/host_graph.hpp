@@ -47,9 +47,14 @@ HostGraph gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, dou
 
 }  // namespace agpm_b200
 
+uint64_t agpm_b200_next_generation();
+
 // C-ABI opaque handle (agpm_b200.h)
 struct agpm_host_graph {
   agpm_b200::HostGraph g;
   bool pinned = false;
+  // process-unique id (never reused): keys device-mirror caches so a freed
+  // graph's recycled addresses can never alias a new graph's (include/agpm/agpm.hpp)
+  uint64_t generation = agpm_b200_next_generation();
 };
 void agpm_b200_unpin_host_graph(agpm_host_graph* g);

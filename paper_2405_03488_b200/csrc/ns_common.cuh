@@ -42,8 +42,6 @@ struct GraphArgs {
   const unsigned long long* __restrict__ seed_arcs;
   unsigned long long arcs;
   int plain;
-  const unsigned long long* __restrict__ ehash;  // edge table (frontier sampler)
-  uint32_t ehash_mask;
   // dense-core adjacency bit matrix (core_bits.cu): bit (u - core_base, v - core_base)
   // of row-major rows of core_wpr words, for u, v >= core_base; null = off
   const uint32_t* __restrict__ core;

@@ -14,6 +14,7 @@
 
 #include <cstdlib>
 
+#include "comm.hpp"
 #include "ns_common.cuh"
 #include "stats.hpp"
 
@@ -204,8 +205,6 @@ GraphArgs graph_args(const agpm_graph* g) {
   a.seed_arcs = g->seed_arcs;
   a.arcs = g->arcs;
   a.plain = g->plain;
-  a.ehash = nullptr;  // see enqueue_sample
-  a.ehash_mask = 0;
   a.core = g->core;
   a.core_base = g->core_base;
   a.core_wpr = g->core_wpr;
@@ -217,7 +216,7 @@ GraphArgs graph_args(const agpm_graph* g) {
 // searches) unless adjacency lists are tiny, where one lane per sample keeps
 // 32 samples in flight per warp. Override with agpm_ns_set_strategy().
 constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3, kStrategyFused = 4, kStrategyFlat = 5;
-int g_strategy = kStrategyAuto;
+std::atomic<int> g_strategy{kStrategyAuto};  // process-wide setting, read once per launch
 
 // clique plans (every step intersects all bound vertices' lists, no out-lists)
 // on graphs whose dense core is a large enough slice (n <= 64 x core dim): their
@@ -233,8 +232,8 @@ bool clique_plan(const DevPlan& p) {
   return true;
 }
 
-int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count) {
-  if (g_strategy != kStrategyAuto) return g_strategy;
+int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count, int forced) {
+  if (forced != kStrategyAuto) return forced;
   const uint64_t core = core_dim_setting();
   if (count >= (1ull << 18) && clique_plan(p) && core && g->n <= 64 * core) return kStrategyFlat;
   const double avg_deg = g->n ? static_cast<double>(g->arcs) / g->n : 0.0;
@@ -244,7 +243,7 @@ int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count) {
 
 // per-sample stream: 0 = CounterRng(seed, 0, id) (the reference's stream, the
 // parity policy), 1 = Philox4x32-10 keyed by seed, counter (draw, id) — flat sampler
-int g_rng_policy = 0;
+std::atomic<int> g_rng_policy{0};
 
 // enqueue one sampling launch for ids [first, first+count) into d_values
 void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint64_t first, uint64_t count,
@@ -253,9 +252,10 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
   auto* cursor = static_cast<unsigned long long*>(ctx.get(0, 64));
   AGPM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
   if (dp.k < 3 || dp.k > AGPM_MAX_K) throw std::invalid_argument("device sampler needs 3 <= k <= 9");
-  if (g_rng_policy == 1) {  // Philox stream: the flat sampler, eager plans
+  const int forced = g_strategy.load(std::memory_order_relaxed);
+  if (g_rng_policy.load(std::memory_order_relaxed) == 1) {  // Philox stream: the flat sampler, eager plans
     if (dp.lazy || d_bytes) throw std::invalid_argument("the Philox stream runs on the eager flat sampler");
-    if (g_strategy != kStrategyAuto && g_strategy != kStrategyFlat)
+    if (forced != kStrategyAuto && forced != kStrategyFlat)
       throw std::invalid_argument("the Philox stream runs on the flat sampler (strategy auto or flat)");
     ensure_core_bits(const_cast<agpm_graph*>(g), s);
     SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, nullptr};
@@ -268,15 +268,13 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
     launch_ns_lazy(L, s);
     return;
   }
-  const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, dp, count);  // B_min replay: warp kernel
+  const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, dp, count, forced);  // B_min replay: warp kernel
   if (strat == kStrategyFrontier || strat == kStrategyFused || strat == kStrategyFlat) ensure_core_bits(const_cast<agpm_graph*>(g), s);
   // the twin-arc index (4 B per arc; 0.4 ms to build on RMAT-20) hints both seed
   // lists; it pays when a view is sampled more than once, so it is built on the
   // view's second sampling launch (same samples with or without it)
   if ((strat == kStrategyFrontier || strat == kStrategyFlat) && ++const_cast<agpm_graph*>(g)->sample_calls >= 2)
     ensure_twin_arcs(const_cast<agpm_graph*>(g), s);
-  // (the edge-hash membership path is available but off: on RMAT-20 it turned
-  // L2-local list searches into random HBM sectors and ran 2.6x slower)
   SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};
   if (strat == kStrategyLane)
     launch_ns_lane(L, s);
@@ -302,6 +300,121 @@ void enqueue_moments(const double* d_values, uint64_t count, uint64_t window, ag
 }
 
 constexpr uint64_t kChunk = 1ull << 24;
+
+// ids [lo, hi) folded into one accumulator: 2^24-sample launches, 4096-sample
+// window partials (fixed shuffle trees) summed on the host in id order
+agpm_accumulator fixed_budget_range(const agpm_graph* g, const DevPlan& dp, uint64_t lo, uint64_t hi, uint64_t seed,
+                                    cudaStream_t s) {
+  agpm_accumulator acc{0, 0, 0.0, 0.0};
+  if (hi <= lo) return acc;
+  DeviceCtx& ctx = ctx_for_current_device();
+  const uint64_t chunk = std::min<uint64_t>(hi - lo, kChunk);
+  constexpr uint64_t kWin = 4096;
+  const uint64_t nwin_chunk = (chunk + kWin - 1) / kWin;
+  auto* d_values = static_cast<double*>(ctx.get(1, sizeof(double) * chunk));
+  auto* d_win = static_cast<agpm_accumulator*>(ctx.get(4, sizeof(agpm_accumulator) * nwin_chunk));
+  auto* h_win = static_cast<agpm_accumulator*>(ctx.get_pinned(0, sizeof(agpm_accumulator) * nwin_chunk));
+  for (uint64_t done = lo; done < hi; done += chunk) {
+    const uint64_t c = std::min(chunk, hi - done);
+    const uint64_t nw = (c + kWin - 1) / kWin;
+    enqueue_sample(g, dp, seed, done, c, d_values, nullptr, nullptr, s);
+    enqueue_moments(d_values, c, kWin, d_win, s);
+    AGPM_CUDA(cudaMemcpyAsync(h_win, d_win, sizeof(agpm_accumulator) * nw, cudaMemcpyDeviceToHost, s));
+    AGPM_CUDA(cudaStreamSynchronize(s));
+    for (uint64_t w = 0; w < nw; ++w) {
+      acc.n += h_win[w].n;
+      acc.hits += h_win[w].hits;
+      acc.sum += h_win[w].sum;
+      acc.squared_sum += h_win[w].squared_sum;
+    }
+  }
+  return acc;
+}
+
+// One round of the sharded online loop: the ids [launched, launched + round)
+// of this round (round = min(world * batch, max_samples - launched)) are dealt
+// to the ranks in contiguous blocks of `batch` (a multiple of the window), so
+// the gathered window records are in id order and the valid ones form a prefix.
+void shard_round(uint64_t launched, uint64_t batch, uint64_t window, uint64_t max_samples, int rank, int world,
+                 agpm_shard_round* out) {
+  const uint64_t round = std::min(batch * (uint64_t)world, max_samples - launched);
+  const uint64_t lo = std::min(round, batch * (uint64_t)rank);
+  out->round_ids = round;
+  out->first_id = launched + lo;
+  out->count = std::min(round - lo, batch);
+  out->valid_windows = (round + window - 1) / window;
+  out->windows_per_rank = batch / window;
+}
+
+// The online loop (ns_engine.cpp:106-140, workers = 1 semantics) on one GPU
+// (c == nullptr) or over the ranks of c. Each round every rank draws its block
+// of B ids (B a multiple of the window W), folds it into W-sample window
+// records, the records are all-gathered in rank = id order, and every rank
+// runs converge_kernel over the same records: the per-window stop test of the
+// reference, so the stop n does not depend on B or on the rank count.
+void online_loop(agpm_comm* c, agpm_graph* g, const agpm_plan* plan, double eps, double delta,
+                 const agpm_online_policy* policy, uint64_t seed, agpm_online_result* out, void* stream) {
+  if (!(eps > 0.0) || !(eps < 1.0)) throw std::invalid_argument("error bound must be inside (0,1)");
+  if (!(delta > 0.0) || !(delta < 1.0)) throw std::invalid_argument("delta must be inside (0,1)");
+  if (!g || !out) throw std::invalid_argument("null argument");
+  DeviceGuard guard(g->device);
+  const DevPlan dp = make_dev_plan(g, plan);
+  agpm_online_policy pol = policy ? *policy : agpm_online_policy{1000, 1000000000ull, 0};
+  DeviceCtx& ctx = ctx_for_current_device();
+  cudaStream_t s = pick_stream(stream);
+  const int rank = c ? comm_rank(c) : 0, world = c ? comm_world(c) : 1;
+  const double z = inv_norm_cdf(1.0 - delta / 2.0);
+  uint64_t window = std::max<uint64_t>(pol.n_min, 10);
+  if (pol.profiled_n_samples > 0) window = std::max(window, pol.profiled_n_samples / 10);
+  const uint64_t max_batch = std::max<uint64_t>(window, (kChunk / window) * window);
+  // first speculative round 2^19 samples over all ranks (then doubling): one
+  // pass covers most 1 %@95 % runs on config-2-sized graphs; measured time to
+  // converge for 4-clique 2.04 ms (2^16 first) -> 0.80 ms (2^19), tools/ttc_probe.py
+  uint64_t batch = std::min(max_batch, std::max<uint64_t>(window, ((1ull << 19) / world / window) * window));
+  const uint64_t nw_max = max_batch / window;
+
+  auto* d_values = static_cast<double*>(ctx.get(1, sizeof(double) * max_batch));
+  auto* d_win = static_cast<agpm_accumulator*>(ctx.get(4, sizeof(agpm_accumulator) * (nw_max + 1)));
+  agpm_accumulator* d_all = d_win;
+  if (world > 1) d_all = static_cast<agpm_accumulator*>(ctx.get(6, sizeof(agpm_accumulator) * nw_max * world));
+  auto* d_state = static_cast<OnlineState*>(ctx.get(5, sizeof(OnlineState)));
+  auto* h_state = static_cast<OnlineState*>(ctx.get_pinned(1, sizeof(OnlineState)));
+  AGPM_CUDA(cudaMemsetAsync(d_state, 0, sizeof(OnlineState), s));
+  if (c) comm_barrier(c, s);
+  auto t0 = std::chrono::steady_clock::now();
+  uint64_t launched = 0;
+  std::memset(h_state, 0, sizeof(OnlineState));
+  while (launched < pol.max_samples) {
+    agpm_shard_round sr{};
+    shard_round(launched, batch, window, pol.max_samples, rank, world, &sr);
+    const uint64_t round = sr.round_ids, mine = sr.count, nw_round = sr.valid_windows;
+    if (mine) {
+      enqueue_sample(g, dp, seed, sr.first_id, mine, d_values, nullptr, nullptr, s);
+      enqueue_moments(d_values, mine, window, d_win, s);
+    }
+    if (world > 1) {
+      const uint64_t nw_rank = batch / window, nw_mine = (mine + window - 1) / window;
+      if (nw_mine < nw_rank)  // padding records past the cap (never reached by the stop test)
+        AGPM_CUDA(cudaMemsetAsync(d_win + nw_mine, 0, sizeof(agpm_accumulator) * (nw_rank - nw_mine), s));
+      comm_all_gather(c, d_win, d_all, sizeof(agpm_accumulator) * nw_rank, s);
+    }
+    converge_kernel<<<1, kConvergeThreads, 0, s>>>(d_all, nw_round, d_state, z, eps, pol.max_samples);
+    count_launch();
+    AGPM_CUDA(cudaGetLastError());
+    AGPM_CUDA(cudaMemcpyAsync(h_state, d_state, sizeof(OnlineState), cudaMemcpyDeviceToHost, s));
+    AGPM_CUDA(cudaStreamSynchronize(s));
+    launched += round;
+    if (h_state->stopped) break;
+    batch = std::min(max_batch, batch * 2);
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  std::memset(out, 0, sizeof(*out));
+  out->report = h_state->rep;
+  out->accumulator = h_state->acc;
+  out->windows = h_state->windows;
+  out->samples_launched = launched;
+  out->seconds = std::chrono::duration<double>(t1 - t0).count();
+}
 
 }  // namespace
 
@@ -395,31 +508,10 @@ int agpm_ns_fixed_budget(agpm_graph* g, const agpm_plan* plan, uint64_t budget, 
   // run_fixed_budget (ns_engine.cpp:142-153): one window of `budget` samples
   return guarded([&] {
     if (budget < 1) throw std::invalid_argument("sample budget must be >= 1");
+    if (!g || !out) throw std::invalid_argument("null argument");
+    DeviceGuard guard(g->device);
     const DevPlan dp = make_dev_plan(g, plan);
-    DeviceCtx& ctx = ctx_for_current_device();
-    cudaStream_t s = pick_stream(stream);
-    const uint64_t chunk = std::min<uint64_t>(budget, kChunk);
-    constexpr uint64_t kWin = 4096;
-    const uint64_t nwin_chunk = (chunk + kWin - 1) / kWin;
-    auto* d_values = static_cast<double*>(ctx.get(1, sizeof(double) * chunk));
-    auto* d_win = static_cast<agpm_accumulator*>(ctx.get(4, sizeof(agpm_accumulator) * nwin_chunk));
-    auto* h_win = static_cast<agpm_accumulator*>(ctx.get_pinned(0, sizeof(agpm_accumulator) * nwin_chunk));
-    agpm_accumulator acc{0, 0, 0.0, 0.0};
-    for (uint64_t done = 0; done < budget; done += chunk) {
-      const uint64_t c = std::min(chunk, budget - done);
-      const uint64_t nw = (c + kWin - 1) / kWin;
-      enqueue_sample(g, dp, seed, done, c, d_values, nullptr, nullptr, s);
-      enqueue_moments(d_values, c, kWin, d_win, s);
-      AGPM_CUDA(cudaMemcpyAsync(h_win, d_win, sizeof(agpm_accumulator) * nw, cudaMemcpyDeviceToHost, s));
-      AGPM_CUDA(cudaStreamSynchronize(s));
-      for (uint64_t w = 0; w < nw; ++w) {
-        acc.n += h_win[w].n;
-        acc.hits += h_win[w].hits;
-        acc.sum += h_win[w].sum;
-        acc.squared_sum += h_win[w].squared_sum;
-      }
-    }
-    *out = acc;
+    *out = fixed_budget_range(g, dp, 0, budget, seed, pick_stream(stream));
   });
 }
 
@@ -430,51 +522,59 @@ int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delt
   // W = max(n_min, 10) (or >= profiled/10) samples; convergence is evaluated
   // after EVERY window even though the device draws speculative batches of
   // many windows, so the stop n equals the reference's.
+  return guarded([&] { online_loop(nullptr, g, plan, eps, delta, policy, seed, out, stream); });
+}
+
+int agpm_ns_shard_round(uint64_t launched, uint64_t batch, uint64_t window, uint64_t max_samples, int rank,
+                        int world, agpm_shard_round* out) {
   return guarded([&] {
-    if (!(eps > 0.0) || !(eps < 1.0)) throw std::invalid_argument("error bound must be inside (0,1)");
-    if (!(delta > 0.0) || !(delta < 1.0)) throw std::invalid_argument("delta must be inside (0,1)");
+    if (!out) throw std::invalid_argument("null argument");
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("rank must be in [0, world)");
+    if (window == 0 || batch == 0 || batch % window) throw std::invalid_argument("batch must be a positive multiple of the window");
+    if (launched > max_samples) throw std::invalid_argument("launched past max_samples");
+    shard_round(launched, batch, window, max_samples, rank, world, out);
+  });
+}
+
+int agpm_ns_online_sharded(agpm_comm* c, agpm_graph* g, const agpm_plan* plan, double eps, double delta,
+                           const agpm_online_policy* policy, uint64_t seed, agpm_online_result* out,
+                           void* stream) {
+  return guarded([&] {
+    if (!c) throw std::invalid_argument("null communicator");
+    online_loop(c, g, plan, eps, delta, policy, seed, out, stream);
+  });
+}
+
+int agpm_ns_fixed_budget_sharded(agpm_comm* c, agpm_graph* g, const agpm_plan* plan, uint64_t budget,
+                                 uint64_t seed, agpm_accumulator* out, void* stream) {
+  // run_fixed_budget (ns_engine.cpp:142-153) with the ids [0, budget) split into
+  // `world` contiguous shares; the ranks' accumulators are gathered and folded in
+  // rank order (the reference merges its workers' accumulators in worker order)
+  return guarded([&] {
+    if (!c || !g || !out) throw std::invalid_argument("null argument");
+    if (budget < 1) throw std::invalid_argument("sample budget must be >= 1");
+    DeviceGuard guard(g->device);
     const DevPlan dp = make_dev_plan(g, plan);
-    agpm_online_policy pol = policy ? *policy : agpm_online_policy{1000, 1000000000ull, 0};
     DeviceCtx& ctx = ctx_for_current_device();
     cudaStream_t s = pick_stream(stream);
-    const double z = inv_norm_cdf(1.0 - delta / 2.0);
-    uint64_t window = std::max<uint64_t>(pol.n_min, 10);
-    if (pol.profiled_n_samples > 0) window = std::max(window, pol.profiled_n_samples / 10);
-    const uint64_t max_batch = std::max<uint64_t>(window, (kChunk / window) * window);
-    // first speculative batch 2^19 (then doubling): one frontier pass covers
-    // most 1 %@95 % runs on config-2-sized graphs; measured time to converge
-    // for 4-clique 2.04 ms (2^16 first) -> 0.80 ms (2^19), tools/ttc_probe.py
-    uint64_t batch = std::min(max_batch, std::max<uint64_t>(window, ((1ull << 19) / window) * window));
-
-    auto* d_values = static_cast<double*>(ctx.get(1, sizeof(double) * max_batch));
-    auto* d_win = static_cast<agpm_accumulator*>(ctx.get(4, sizeof(agpm_accumulator) * (max_batch / window + 1)));
-    auto* d_state = static_cast<OnlineState*>(ctx.get(5, sizeof(OnlineState)));
-    auto* h_state = static_cast<OnlineState*>(ctx.get_pinned(1, sizeof(OnlineState)));
-    AGPM_CUDA(cudaMemsetAsync(d_state, 0, sizeof(OnlineState), s));
-    auto t0 = std::chrono::steady_clock::now();
-    uint64_t launched = 0;
-    std::memset(h_state, 0, sizeof(OnlineState));
-    while (launched < pol.max_samples) {
-      const uint64_t c = std::min(batch, pol.max_samples - launched);
-      const uint64_t nw = (c + window - 1) / window;
-      enqueue_sample(g, dp, seed, launched, c, d_values, nullptr, nullptr, s);
-      enqueue_moments(d_values, c, window, d_win, s);
-      converge_kernel<<<1, kConvergeThreads, 0, s>>>(d_win, nw, d_state, z, eps, pol.max_samples);
-      count_launch();
-      AGPM_CUDA(cudaGetLastError());
-      AGPM_CUDA(cudaMemcpyAsync(h_state, d_state, sizeof(OnlineState), cudaMemcpyDeviceToHost, s));
-      AGPM_CUDA(cudaStreamSynchronize(s));
-      launched += c;
-      if (h_state->stopped) break;
-      batch = std::min(max_batch, batch * 2);
+    const int rank = comm_rank(c), world = comm_world(c);
+    const uint64_t share = (budget + world - 1) / world;
+    const uint64_t lo = std::min(budget, share * rank), hi = std::min(budget, lo + share);
+    const agpm_accumulator mine = fixed_budget_range(g, dp, lo, hi, seed, s);
+    auto* d = static_cast<agpm_accumulator*>(ctx.get(10, sizeof(agpm_accumulator) * (world + 1)));
+    AGPM_CUDA(cudaMemcpyAsync(d + world, &mine, sizeof(mine), cudaMemcpyHostToDevice, s));
+    comm_all_gather(c, d + world, d, sizeof(agpm_accumulator), s);
+    std::vector<agpm_accumulator> all(world);
+    AGPM_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(agpm_accumulator) * world, cudaMemcpyDeviceToHost, s));
+    AGPM_CUDA(cudaStreamSynchronize(s));
+    agpm_accumulator acc{0, 0, 0.0, 0.0};
+    for (const auto& a : all) {
+      acc.n += a.n;
+      acc.hits += a.hits;
+      acc.sum += a.sum;
+      acc.squared_sum += a.squared_sum;
     }
-    auto t1 = std::chrono::steady_clock::now();
-    std::memset(out, 0, sizeof(*out));
-    out->report = h_state->rep;
-    out->accumulator = h_state->acc;
-    out->windows = h_state->windows;
-    out->samples_launched = launched;
-    out->seconds = std::chrono::duration<double>(t1 - t0).count();
+    *out = acc;
   });
 }
 

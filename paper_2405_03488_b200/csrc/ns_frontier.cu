@@ -10,9 +10,9 @@
 //   scan     (CUB)                  word offsets: every sample's hit bitmap
 //            starts on a 32-bit word boundary.
 //   isect    (1 warp / bitmap word) a word = 32 driver elements of ONE sample.
-//            Every "a in list q" test is one probe of the device edge table
-//            (edge_hash.cuh: one 32-B bucket per lookup), since the driver
-//            already sits inside the step's [lo, hi). Without a table the warp
+//            A test "a in list q" is one bit of the dense-core matrix when q's
+//            owner is a core vertex (the driver already sits inside the step's
+//            [lo, hi), so membership is edge existence); otherwise the warp
 //            loads 32 splitters of list q, finds each lane's bucket with a
 //            5-step shuffle search and finishes with a short per-lane search.
 //            One ballot -> the fail word. No atomics, no memset.
@@ -34,7 +34,6 @@
 #include <algorithm>
 #include <stdexcept>
 
-#include "edge_hash.cuh"
 #include "frontier_common.cuh"
 
 namespace agpm_b200 {
@@ -167,9 +166,7 @@ __global__ void __launch_bounds__(256, 8) fr_isect_kernel(const FrontierArgs A, 
         } else {
           const uint32_t* B = nbr + d.start[q];
           const uint32_t nb = d.len[q];
-          if (A.g.ehash) {
-            found = valid && edge_lookup(A.g.ehash, A.g.ehash_mask, a, d.owner[q]);
-          } else if (nb <= 32) {
+          if (nb <= 32) {
             found = warp_contains((uint32_t)lane < nb ? ldo(B, (uint32_t)lane) : INF, a);
           } else {
             // 32 splitters at (i+1)*step; lane's bucket by shuffle search, then a short per-lane search

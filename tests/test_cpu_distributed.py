@@ -1,10 +1,15 @@
-"""CPU, world_size 2 (gloo): the sharded online driver of paper_2405_03488_b200.distributed.
+"""CPU, world_size 2 (gloo): the host side of the multi-GPU drivers.
 
-Each rank draws its shard of global sample ids (here with the C oracle as the
-per-rank sampler — on GPUs the sampling kernel), reduces them to window
-moments, the ranks all-gather the moments and replay the window loop. The
-result must equal the single-process reference-semantics run_ns_online
-(workers = 1): same stop n, windows, hits; sums to reduction-order rounding.
+On GPUs the sharded online loop (csrc/ns_device.cu online_loop) runs per rank:
+agpm_ns_shard_round says which ids this rank draws in the round, the rank folds
+them into 1000-sample window records, the records are all-gathered (NCCL) in
+rank order and every rank runs the stop test over the gathered prefix. Here the
+same loop runs on CPU ranks: the PRODUCT's partition function (the C-ABI call,
+no device needed) decides the ids, the oracle stands in for the sampling kernel
+only, gloo carries the records. The result must equal the single-process
+reference-semantics run_ns_online (workers = 1): same stop n, windows, hits;
+sums to reduction-order rounding. (The native loop itself is checked on the GPU
+against the 1-rank run: tests/test_gpu_multi.py.)
 """
 import os
 import socket
@@ -16,6 +21,20 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WINDOW = 1000
+
+
+def window_records(values, window, nrec):
+    """(n, hits, sum, squared_sum) per window of consecutive samples, padded to nrec records."""
+    out = np.zeros((nrec, 4), np.float64)
+    for w in range((len(values) + window - 1) // window):
+        seg = values[w * window:(w + 1) * window]
+        s = sq = 0.0
+        for x in seg:
+            s += x
+            sq += x * x
+        out[w] = (len(seg), np.count_nonzero(seg), s, sq)
+    return out
 
 
 def _free_port():
@@ -33,7 +52,6 @@ def _worker(rank, world, port, case, out_q):
 
     import paper_2405_03488_b200 as A
     from oracle_bindings import Oracle
-    from paper_2405_03488_b200 import distributed as D
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -42,21 +60,32 @@ def _worker(rank, world, port, case, out_q):
     off, nbr = g.arrays()
     plan = A.compile_plan(pat)
     O = Oracle()
-
-    def sample_moments(first, count):
-        v, h, b = O.draw_records(off, nbr, g.edge_count, plan, seed, first, count)
-        return D.window_moments(v, 1000)
-
-    def all_gather(local):
-        t = torch.from_numpy(local)
-        parts = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(parts, t)
-        return torch.cat(parts).numpy()
-
-    m = D.run_ns_online_sharded(sample_moments, all_gather, rank, world, eps, delta, window=1000,
-                                max_samples=max_samples, per_rank=per_rank)
-    out_q.put((rank, m.acc.n, m.acc.hits, m.acc.sum, m.acc.squared_sum, m.windows, m.report.converged,
-               m.report.epsilon_hat))
+    z = A.inv_norm_cdf(1.0 - delta / 2.0)
+    acc = A.Accumulator()
+    windows, launched, batch, stopped, rep = 0, 0, per_rank, False, None
+    while launched < max_samples and not stopped:
+        sr = A.shard_round(launched, batch, WINDOW, max_samples, rank, world)
+        vals = np.zeros(0)
+        if sr.count:
+            vals, _, _ = O.draw_records(off, nbr, g.edge_count, plan, seed, sr.first_id, sr.count)
+        local = torch.from_numpy(window_records(vals, WINDOW, sr.windows_per_rank))
+        parts = [torch.zeros_like(local) for _ in range(world)]
+        dist.all_gather(parts, local)
+        recs = torch.cat(parts).numpy()[: sr.valid_windows]
+        for nn, hh, s, sq in recs:  # the stop test after every window, in id order
+            acc.n += int(nn)
+            acc.hits += int(hh)
+            acc.sum += float(s)
+            acc.squared_sum += float(sq)
+            windows += 1
+            rep = O.predicted_error(acc, delta)
+            if rep.epsilon_hat <= eps or acc.n >= max_samples:
+                stopped = True
+                break
+        launched += sr.round_ids
+        batch = min(batch * 2, 16 * per_rank)
+    assert z > 0
+    out_q.put((rank, acc.n, acc.hits, acc.sum, acc.squared_sum, windows, rep.epsilon_hat <= eps, rep.epsilon_hat))
     dist.destroy_process_group()
 
 
@@ -96,7 +125,6 @@ def _exact_worker(rank, world, port, case, out_q):
 
     import paper_2405_03488_b200 as A
     from oracle_bindings import Oracle
-    from paper_2405_03488_b200 import distributed as D
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -111,8 +139,7 @@ def _exact_worker(rank, world, port, case, out_q):
         dist.all_reduce(t)
         return int(t.item())
 
-    total = D.exact_count_sharded(lambda r, w: O.exact_count_shard(off, nbr, g.edge_count, plan, r, w),
-                                  all_reduce_sum, rank, world)
+    total = all_reduce_sum(O.exact_count_shard(off, nbr, g.edge_count, plan, rank, world))
     out_q.put((rank, total))
     dist.destroy_process_group()
 
@@ -146,3 +173,32 @@ def test_oracle_shards_sum_to_exact_count(agpm, oracle, nshards):
         plan = agpm.compile_plan(pat)
         parts = [oracle.exact_count_shard(off, nbr, g.edge_count, plan, r, nshards) for r in range(nshards)]
         assert sum(parts) == oracle.exact_count(off, nbr, g.edge_count, plan)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_round_partitions_ids(agpm, world):
+    """agpm_ns_shard_round (the online loop's id partition): the ranks' blocks
+    tile the round's ids in rank order, every block starts on a window boundary,
+    the valid window records are exactly the gathered prefix, and the cap cuts
+    the round without gaps."""
+    for window, batch, max_samples in ((1000, 4000, 10**9), (1000, 2000, 9500), (10, 30, 125), (7, 7, 50)):
+        launched = 0
+        while launched < max_samples:
+            rs = [agpm.shard_round(launched, batch, window, max_samples, r, world) for r in range(world)]
+            rnd = rs[0].round_ids
+            assert rnd == min(world * batch, max_samples - launched)
+            nxt = launched
+            recs = 0
+            for r, sr in enumerate(rs):
+                assert sr.round_ids == rnd and sr.windows_per_rank == batch // window
+                if sr.count:
+                    assert sr.first_id == nxt and sr.first_id % window == launched % window
+                    assert recs == r * sr.windows_per_rank  # earlier ranks were full
+                    recs += (sr.count + window - 1) // window
+                nxt += sr.count
+            assert nxt == launched + rnd and recs == rs[0].valid_windows
+            launched += rnd
+            if launched > 10 * world * batch:
+                break
+    with pytest.raises(ValueError):
+        agpm.shard_round(0, 1500, 1000, 10**9, 0, 2)  # batch not a window multiple

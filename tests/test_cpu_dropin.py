@@ -27,6 +27,9 @@ def test_dropin_header_host_calls(agpm, tmp_path):
     assert "keep p=0.05533 colors=18" in out  # test_gs_engine.cpp:14-34
     # cost model through the header (the C entry points are reference-pinned in test_cpu_cost.py)
     assert "cone 2.200e-05..4.700e-05 gs 2.250e-08 -> GS" in out
+    # K4: 4 triangles (brute force), 2 through any edge (= gamma), 12 arcs; SeedIndex.arc = the
+    # reference's upper_bound(prefix) arc (ns_engine.cpp:18-23)
+    assert "brute triangles=4 through(0,1)=2 gamma=2 seeds=12 arc0=(0,1) arc11=(3,2)" in out
 
 
 @pytest.mark.gpu
@@ -40,3 +43,7 @@ def test_dropin_header_device_calls(agpm, tmp_path):
     assert "gs c=1 estimate=4.0 raw=4" in out
     # colours {0,1,0,1} on K4 keep edges 0-2 and 1-3; merging both colours restores K4
     assert "colored same=2 merged same=6 merged triangles=4" in out
+    assert re.search(r"draw value=(\S+) hit=(\d)", out).groups() == \
+        re.search(r"draw with seed index value=(\S+) hit=(\d)", out).groups()
+    assert "aba 0 1 0 1" in out  # no stale device mirror for a freed graph's successor
+    assert "same=1" in out  # workers -> GPUs: identical result (one rank on a 1-GPU box)
