@@ -128,8 +128,6 @@ def test_gs_online_replay_and_bound(agpm, oracle, pattern, colors):
     the accumulated estimates and the report equal a host replay of the same
     colourings (gs_estimate with seeds derive_key(seed, i, 0)) through the
     reference's window rule, and the estimate sits within 3 eps of the exact count."""
-    from paper_2405_03488_b200.distributed import _inv_norm_cdf, predicted_error_py
-
     g = agpm.er_graph(400, 0.05, 8).relabel_by_degree()
     dg = agpm.DeviceGraph(g)
     plan = agpm.compile_plan(pattern)
@@ -137,13 +135,12 @@ def test_gs_online_replay_and_bound(agpm, oracle, pattern, colors):
     eps, delta, seed = 0.05, 0.05, 3
     r = agpm.gs_online(dg, plan, colors, eps, delta, max_colorings=4000, seed=seed)
     assert r.report.converged and 2 <= r.windows < 4000
-    z = _inv_norm_cdf(1.0 - delta / 2.0)
     s = sq = 0.0
     for i in range(r.windows):
         x = agpm.gs_estimate(dg, plan, "color", colors=colors, seed=oracle.L.orc_derive_key(seed, i, 0)).estimate
         s += x
         sq += x * x
-        rep = predicted_error_py(i + 1, 0, s, sq, z)
+        rep = oracle.predicted_error(agpm.Accumulator(i + 1, 0, s, sq), delta)
         assert (rep.epsilon_hat <= eps) == (i + 1 == r.windows)
     assert s == r.accumulator.sum and sq == r.accumulator.squared_sum and r.report.mu == s / r.windows
     assert abs(r.report.mu - exact) <= 3 * eps * exact
