@@ -220,11 +220,10 @@ int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delt
 /* Sampler strategy: 0 = auto (default), 1 = one warp per sample
  * (k-ary searches + coalesced chunk intersections), 2 = one lane per sample
  * (tiny adjacency lists), 3 = frontier phases (element-parallel
- * intersections over a whole batch), 4 = fused (a warp owns 32 samples: scalar
- * work lane-parallel, intersections warp-cooperative, state kept on chip),
- * 5 = flat (a warp owns 32 samples, state on chip; each multi-list step
+ * intersections over a whole batch), 5 = flat (a warp owns 32 samples, state on chip; each multi-list step
  * intersects the concatenation of the pending samples' drivers element-parallel,
- * picks lane-parallel). All strategies draw identical samples. */
+ * picks lane-parallel). All strategies draw identical samples. (4, a fused
+ * warp-per-sample-group sampler, was removed: slower than 3 and 5 everywhere.) */
 int agpm_ns_set_strategy(int strategy);
 /* Per-sample stream policy: 0 = CounterRng(seed, 0, sample_id) (default; the
  * reference's stream, bit-exact with its draw_sample), 1 = Philox4x32-10 keyed by

@@ -34,7 +34,8 @@ __all__ = [
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libagpm_b200.so")
+# AGPM_LIB: a side build of the same sources (csrc/Makefile SUFFIX=...) for A/B timing
+LIB_PATH = os.environ.get("AGPM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libagpm_b200.so")
 
 
 class AgpmError(RuntimeError):
@@ -643,11 +644,11 @@ def window_moments_dev(d_values_ptr, count, window, d_out_ptr, stream=None):
                                          None if stream is None else C.c_void_p(stream)))
 
 
-STRATEGIES = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3, "fused": 4, "flat": 5}
+STRATEGIES = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3, "flat": 5}
 
 
 def set_strategy(name):
-    """Sampler kernel choice (all draw identical samples): auto | warp | lane | frontier | fused."""
+    """Sampler kernel choice (all draw identical samples): auto | warp | lane | frontier | flat."""
     _check(lib().agpm_ns_set_strategy(STRATEGIES[name]))
 
 

@@ -1,6 +1,6 @@
 // Per-sample state, step descriptors and the lane-level step logic shared by
 // the frontier (phase) sampler (ns_frontier.cu) and the on-chip samplers
-// (fused: ns_frontier.cu, flat: ns_flat.cu).
+// (flat: ns_flat.cu).
 #pragma once
 
 #include "ns_common.cuh"
@@ -182,7 +182,7 @@ __device__ __forceinline__ void step_bounds(const DevPlan& p, int s, const Sampl
 // `surv` set, step s0 uses those survivors of step s0-1 as its driver and only
 // the lists step s0-1 did not have.
 // Returns the step whose descriptor was written (pending intersection), or -1
-// once the sample is finished. With `local` set (fused kernel) the descriptor
+// once the sample is finished. With `local` set (flat kernel) the descriptor
 // goes there and nothing is written to the SoA state.
 template <int K, class R>
 __device__ int advance(const FrontierArgs& A, unsigned long long i, Sample<K, R>& S, int s0, const uint32_t* surv,

@@ -160,7 +160,6 @@ void launch_ns_lane(const SampleLaunch& L, cudaStream_t s);
 void launch_ns_warp(const SampleLaunch& L, cudaStream_t s);
 void launch_ns_frontier(const SampleLaunch& L, cudaStream_t s);
 void launch_ns_lazy(const SampleLaunch& L, cudaStream_t s);
-void launch_ns_fused(const SampleLaunch& L, cudaStream_t s);
 void launch_ns_flat(const SampleLaunch& L, cudaStream_t s, bool philox = false);
 void set_frontier_reuse(bool on);
 

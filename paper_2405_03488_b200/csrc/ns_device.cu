@@ -215,7 +215,8 @@ GraphArgs graph_args(const agpm_graph* g) {
 // Strategy: one warp per sample (coalesced chunk intersections, k-ary
 // searches) unless adjacency lists are tiny, where one lane per sample keeps
 // 32 samples in flight per warp. Override with agpm_ns_set_strategy().
-constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3, kStrategyFused = 4, kStrategyFlat = 5;
+// (4 was the fused sampler: measured slower than flat and frontier everywhere, removed)
+constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3, kStrategyFlat = 5;
 std::atomic<int> g_strategy{kStrategyAuto};  // process-wide setting, read once per launch
 
 // clique plans (every step intersects all bound vertices' lists, no out-lists)
@@ -269,7 +270,7 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
     return;
   }
   const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, dp, count, forced);  // B_min replay: warp kernel
-  if (strat == kStrategyFrontier || strat == kStrategyFused || strat == kStrategyFlat) ensure_core_bits(const_cast<agpm_graph*>(g), s);
+  if (strat == kStrategyFrontier || strat == kStrategyFlat) ensure_core_bits(const_cast<agpm_graph*>(g), s);
   // the twin-arc index (4 B per arc; 0.4 ms to build on RMAT-20) hints both seed
   // lists; it pays when a view is sampled more than once, so it is built on the
   // view's second sampling launch (same samples with or without it)
@@ -280,8 +281,6 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
     launch_ns_lane(L, s);
   else if (strat == kStrategyFrontier)
     launch_ns_frontier(L, s);
-  else if (strat == kStrategyFused)
-    launch_ns_fused(L, s);
   else if (strat == kStrategyFlat)
     launch_ns_flat(L, s);
   else
@@ -426,8 +425,8 @@ extern "C" {
 
 int agpm_ns_set_strategy(int strategy) {
   return guarded([&] {
-    if (strategy < 0 || strategy > 5)
-      throw std::invalid_argument("strategy must be 0 (auto), 1 (warp), 2 (lane), 3 (frontier), 4 (fused) or 5 (flat)");
+    if (strategy < 0 || strategy > 5 || strategy == 4)
+      throw std::invalid_argument("strategy must be 0 (auto), 1 (warp), 2 (lane), 3 (frontier) or 5 (flat)");
     g_strategy = strategy;
   });
 }

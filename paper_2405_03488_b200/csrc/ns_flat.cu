@@ -32,6 +32,9 @@ namespace {
 // is |S_j| directly.
 constexpr int kFlatW = 64;  // ballot words per warp and round (drivers up to 2048 elements go flat)
 constexpr int kFlatThreads = 128;
+#ifndef AGPM_FLAT_U
+#define AGPM_FLAT_U 2  // driver words in flight per warp in the fast loop
+#endif
 
 template <int K>
 __device__ __forceinline__ bool flat_live(const GraphArgs& g, const IsectDesc<K>& d, uint32_t a) {
@@ -337,7 +340,7 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
   // regs 14.2 ms, 64 regs 9.1, 56 regs 8.9, 48 regs 8.8, 40 regs 9.9; triangle
   // 64 regs 5.5 vs 48 regs 5.8; 5-clique 48 regs 12.3 vs 64 regs 13.4.
   constexpr int kMinB = K == 3 ? 8 : K <= 5 ? 10 : 8;
-  auto kern = fr_flat_kernel<K, 2, kMinB, R>;
+  auto kern = fr_flat_kernel<K, AGPM_FLAT_U, kMinB, R>;
   static int occ = -1;
   if (occ < 0) {
     int o = 0;

@@ -319,132 +319,6 @@ __global__ void __launch_bounds__(256) fr_pick_kernel(const FrontierArgs A, int 
   }
 }
 
-// Fused sampler: one warp owns 32 samples (lane l <-> sample base + l).
-// Scalar work (seed, bounds, ranges, driver choice, single-list steps) runs
-// lane-parallel exactly as in fr_seed/fr_pick; each lane leaves its step
-// descriptor in shared memory, and the warp then intersects the pending
-// samples one after another, all 32 lanes on one sample's driver words (core
-// bit tests or splitter searches, as in fr_isect), counts |S_j| from the live
-// ballots, draws r with that sample's own CounterRng (broadcast, evaluated
-// uniformly) and selects the r-th live element from the per-lane ballot words.
-// No per-sample state leaves the SM between steps: no SoA state, scans,
-// bitmaps or host round trips.
-template <int K>
-__global__ void __launch_bounds__(256) fr_fused_kernel(const FrontierArgs A) {
-  __shared__ IsectDesc<K> sdesc[256];
-  const int lane = threadIdx.x & 31;
-  IsectDesc<K>* wdesc = sdesc + (threadIdx.x & ~31u);
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long base = (blockIdx.x * (unsigned long long)blockDim.x) + (threadIdx.x & ~31u);
-       base < A.count; base += stride) {
-    const unsigned long long i = base + lane;
-    const bool act = i < A.count;
-    Sample<K> S(A.seed, A.first_id + (act ? i : 0));
-    int pend = -1;
-    if (act) {
-      S.alpha = A.p.alpha0;
-      const unsigned long long r0 = S.rng.next_below(A.g.arcs);  // ns_engine.cpp:29-33
-      const unsigned long long arc = __ldg(A.g.seed_arcs + r0);
-      uint32_t u = (uint32_t)(arc >> 32), v = (uint32_t)arc;
-      const bool swapped = A.p.seed_ordered && u > v;
-      if (swapped) {
-        const uint32_t t = u;
-        u = v;
-        v = t;
-      }
-      bind(S, 0, u);
-      bind(S, 1, v);
-      ensure_vtx(A.g, S, 0);
-      ensure_vtx(A.g, S, 1);
-      if (A.g.plain) {
-        if (!swapped) {
-          S.hbo[0] = (uint32_t)(r0 - S.pb[0]) + 1;
-          S.hbl[0] = v + 1;
-        } else {
-          S.hbo[1] = (uint32_t)(r0 - S.pb[1]) + 1;
-          S.hbl[1] = u + 1;
-        }
-      }
-      pend = advance<K>(A, i, S, 0, nullptr, 0, wdesc + lane);
-    }
-    for (;;) {
-      unsigned pending = __ballot_sync(FULL, pend >= 0);
-      if (!pending) break;
-      __syncwarp();
-      bool picked = false;
-      while (pending) {
-        const int src = __ffs(pending) - 1;
-        pending &= pending - 1;
-        const int step = __shfl_sync(FULL, pend, src);
-        const int j = step + 2;
-        const IsectDesc<K>& d = wdesc[src];
-        const uint32_t core = d.core;
-        const uint32_t nw = (d.dsize + 31) >> 5;
-        unsigned myword = 0;
-        unsigned long long cnt = 0;
-        for (uint32_t w = 0; w < nw; ++w) {
-          const unsigned live = live_word<K>(A, d, core, w, lane, j);
-          if ((uint32_t)lane == w) myword = live;
-          cnt += __popc(live);
-        }
-        if (cnt == 0) {
-          if (lane == src) {
-            finish(A, i, S, j, false);
-            pend = -1;
-          }
-          continue;
-        }
-        CounterRng rr(0);
-        rr.key = __shfl_sync(FULL, S.rng.key, src);
-        rr.ctr = __shfl_sync(FULL, S.rng.ctr, src);
-        unsigned long long r = rr.next_below(cnt);  // uniform: every lane runs src's stream
-        uint32_t o_pick = 0;
-        if (nw <= 32) {
-          const unsigned pc = __popc(myword);
-          unsigned incl = pc;
-#pragma unroll
-          for (int dd = 1; dd < 32; dd <<= 1) {
-            const unsigned t = __shfl_up_sync(FULL, incl, dd);
-            if (lane >= dd) incl += t;
-          }
-          const unsigned excl = incl - pc;
-          const unsigned who = __ballot_sync(FULL, excl <= r && r < incl);
-          const int wl = __ffs(who) - 1;
-          uint32_t ob = 0;
-          if (lane == wl) ob = (uint32_t)wl * 32 + __fns(myword, 0, (int)(r - excl) + 1);
-          o_pick = __shfl_sync(FULL, ob, wl);
-        } else {  // long driver: replay the words up to the r-th live element
-          for (uint32_t w = 0; w < nw; ++w) {
-            const unsigned live = live_word<K>(A, d, core, w, lane, j);
-            const unsigned pc = __popc(live);
-            if (r < pc) {
-              o_pick = w * 32 + __fns(live, 0, (int)r + 1);
-              break;
-            }
-            r -= pc;
-          }
-        }
-        const uint32_t pick = ldo(d.drv, o_pick);
-        if (lane == src) {
-          S.rng.ctr = rr.ctr;
-          S.alpha = __dmul_rn(S.alpha, (double)cnt);  // alpha *= |S_j| (ns_engine.cpp:39)
-          if (d.drv_pos != NO_DRV) {
-#pragma unroll
-            for (int q = 0; q < K; ++q)
-              if ((uint32_t)q == d.drv_pos) {  // lower_bound(pick + 1) = drv_rs + o + 1
-                S.hbo[q] = d.drv_rs + o_pick + 1;
-                S.hbl[q] = pick + 1;
-              }
-          }
-          bind(S, j, pick);
-          picked = true;
-        }
-      }
-      __syncwarp();
-      if (picked) pend = advance<K>(A, i, S, pend + 1, nullptr, 0, wdesc + lane);
-    }
-  }
-}
 
 // Nested survivor reuse is exact but, at word granularity, rarely cheaper than
 // re-intersecting (a sample's step-j driver is ~1 bitmap word either way) while
@@ -546,54 +420,12 @@ void run_frontier_k(const SampleLaunch& L, cudaStream_t s) {
   }
 }
 
-template <int K>
-void run_fused_k(const SampleLaunch& L, cudaStream_t s) {
-  DeviceCtx& ctx = ctx_for_current_device();
-  FrontierArgs A{};
-  A.g = L.g;
-  A.p = L.p;
-  A.seed = L.seed;
-  A.first_id = L.first_id;
-  A.count = L.count;
-  A.values = L.values;
-  A.bindings = L.bindings;
-  for (int st = 0; st < K - 2; ++st) {
-    const unsigned in_m = L.p.in_mask[st], out_m = L.p.out_mask[st];
-    A.step_multi[st] = !(__builtin_popcount(in_m) == 1 && out_m == 0);
-    A.step_reuse[st] = 0;
-  }
-  static int occ = -1;
-  if (occ < 0) {
-    int o = 0;
-    AGPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fr_fused_kernel<K>, 256, 0));
-    occ = o > 0 ? o : 1;
-  }
-  const unsigned blocks =
-      (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>((L.count + 255) / 256,
-                                                                             (unsigned long long)ctx.sm_count * occ));
-  fr_fused_kernel<K><<<blocks, 256, 0, s>>>(A);
-  count_launch();
-  AGPM_CUDA(cudaGetLastError());
-}
 
 
 }  // namespace
 
 void set_frontier_reuse(bool on) { g_frontier_reuse = on; }
 
-void launch_ns_fused(const SampleLaunch& L, cudaStream_t s) {
-  if (L.bytes_out) throw std::invalid_argument("B_min accounting runs on the warp sampler");
-  switch (L.p.k) {
-    case 3: run_fused_k<3>(L, s); break;
-    case 4: run_fused_k<4>(L, s); break;
-    case 5: run_fused_k<5>(L, s); break;
-    case 6: run_fused_k<6>(L, s); break;
-    case 7: run_fused_k<7>(L, s); break;
-    case 8: run_fused_k<8>(L, s); break;
-    case 9: run_fused_k<9>(L, s); break;
-    default: throw std::invalid_argument("device sampler needs 3 <= k <= 9");
-  }
-}
 
 void launch_ns_frontier(const SampleLaunch& L, cudaStream_t s) {
   if (L.bytes_out) throw std::invalid_argument("B_min accounting runs on the warp sampler");

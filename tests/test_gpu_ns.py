@@ -36,7 +36,7 @@ def graphs(agpm):
     return _graphs(agpm)
 
 
-@pytest.fixture(params=["warp", "lane", "frontier", "frontier_reuse", "frontier_nocore", "fused", "fused_nocore", "flat",
+@pytest.fixture(params=["warp", "lane", "frontier", "frontier_reuse", "frontier_nocore", "flat",
                         "flat_nocore", "flat_core96", "frontier_core96"])
 def strategy(agpm, request):
     agpm.set_strategy(request.param.split("_")[0])
