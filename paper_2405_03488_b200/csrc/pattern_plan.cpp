@@ -1,24 +1,25 @@
 // Pattern model and plan compiler (host side of the hot path, SURVEY §8(a)
-// row 10). Produces agpm_plan, the field-for-field image of the reference's
-// ExecutionPlan (plan.hpp:34-55). The compile rules follow plan.cpp:57-137:
-//   * seed = pattern edge with the largest endpoint-degree sum, higher-degree
-//     endpoint first (plan.cpp:40-53);
-//   * remaining vertices by most already-bound neighbours, ties to the smaller
-//     id (plan.cpp:62-76);
-//   * Grochow-Kellis orbit constraints walked in matching order
-//     (plan.cpp:20-38);
-//   * eager steps: in-lists = bound pattern neighbours, out-lists for
-//     vertex-induced patterns, order bounds at the later endpoint; lazy
-//     steps: tree parent + closure + terminal constraints.
-// tests/test_plan.py checks every builtin x mode x symmetry against plans
-// dumped from the reference itself (tests/golden/plans.json).
+// row 10). Output: agpm_plan, the field-for-field image of the reference's
+// ExecutionPlan (plan.hpp:34-55); tests/test_cpu_host.py checks every builtin x
+// verify mode x symmetry setting, custom specs and the error messages against
+// plans dumped from the compiled reference (tests/golden/plans.json).
+//
+// Everything is done on adjacency bitmasks (k <= 9, one u32 row per pattern
+// vertex): the edge list is the set bits of the upper triangle in row order
+// (= the reference's sorted, de-duplicated edge list, pattern.cpp:24-41), the
+// automorphism group comes from a pruned backtracking search over partial
+// permutations instead of scanning all k! orderings (pattern.cpp:43-57 tests
+// every permutation), orbits and stabilisers are masks over that group
+// (Grochow-Kellis, plan.cpp:20-38), and the matching order is a greedy
+// max-popcount choice over the bound mask (plan.cpp:40-76). Interface
+// behaviour — plan contents, element order of every list, error texts — is
+// the reference's; the implementation is not.
 
 #include <algorithm>
+#include <array>
+#include <cctype>
 #include <cstdio>
 #include <cstring>
-#include <map>
-#include <set>
-#include <sstream>
 #include <string>
 #include <vector>
 
@@ -28,302 +29,313 @@ namespace agpm_b200 {
 
 namespace {
 
-struct Pattern {
+using Perm = std::array<int8_t, AGPM_MAX_K>;
+
+struct Shape {
   std::string name;
   int k = 0;
-  std::vector<std::pair<int, int>> edges;
-  bool vertex_induced = false;
-  std::vector<uint32_t> adj;
+  uint32_t row[AGPM_MAX_K] = {};  // row[v] bit u <=> edge {u, v}
+  bool induced = false;
 
-  bool has_edge(int a, int b) const { return (adj[a] >> b) & 1u; }
-  int degree(int v) const { return __builtin_popcount(adj[v]); }
-  bool is_clique() const { return static_cast<int>(edges.size()) == k * (k - 1) / 2; }
-
-  bool connected() const {  // pattern.cpp:10-22
-    if (k == 0) return false;
-    uint32_t reached = 1, frontier = 1;
-    while (frontier) {
-      uint32_t next = 0;
-      for (int v = 0; v < k; ++v)
-        if ((frontier >> v) & 1u) next |= adj[v];
-      frontier = next & ~reached;
-      reached |= next;
-    }
-    return reached == (1u << k) - 1;
+  bool edge(int a, int b) const { return (row[a] >> b) & 1u; }
+  int deg(int v) const { return __builtin_popcount(row[v]); }
+  int edge_count() const {
+    int m = 0;
+    for (int v = 0; v < k; ++v) m += deg(v);
+    return m / 2;
   }
-
-  void normalize() {  // pattern.cpp:24-41
-    if (k < 2 || k > 9) throw pattern_error("pattern must have between 2 and 9 vertices");
-    for (auto& [a, b] : edges) {
-      if (a == b) throw pattern_error("pattern has a self-loop");
-      if (a < 0 || b < 0 || a >= k || b >= k) throw pattern_error("pattern edge endpoint out of range");
-      if (a > b) std::swap(a, b);
-    }
-    std::sort(edges.begin(), edges.end());
-    edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
-    adj.assign(k, 0);
-    for (auto [a, b] : edges) {
-      adj[a] |= 1u << b;
-      adj[b] |= 1u << a;
-    }
-    if (!connected()) throw pattern_error("pattern must be connected");
-  }
-
-  // every permutation preserving the edge set (pattern.cpp:43-57)
-  std::vector<std::vector<int>> automorphisms() const {
-    std::vector<int> perm(k);
-    for (int i = 0; i < k; ++i) perm[i] = i;
-    std::vector<std::vector<int>> out;
-    do {
-      bool ok = true;
-      for (auto [a, b] : edges)
-        if (!has_edge(perm[a], perm[b])) {
-          ok = false;
-          break;
-        }
-      if (ok) out.push_back(perm);
-    } while (std::next_permutation(perm.begin(), perm.end()));
-    return out;
+  // visit edges (a < b) in ascending (a, b) order
+  template <class F>
+  void each_edge(F&& f) const {
+    for (int a = 0; a < k; ++a)
+      for (uint32_t up = row[a] >> (a + 1), b = a + 1; up; up >>= 1, ++b)
+        if (up & 1u) f(a, static_cast<int>(b));
   }
 };
 
-Pattern make(const std::string& name, int k, std::vector<std::pair<int, int>> edges, bool vinduced) {
-  Pattern p;
-  p.name = name;
-  p.k = k;
-  p.edges = std::move(edges);
-  p.vertex_induced = vinduced;
-  p.normalize();
-  return p;
-}
-
-std::vector<std::pair<int, int>> clique(int k) {
-  std::vector<std::pair<int, int>> e;
-  for (int a = 0; a < k; ++a)
-    for (int b = a + 1; b < k; ++b) e.emplace_back(a, b);
-  return e;
-}
-
-std::vector<std::pair<int, int>> path(int k) {
-  std::vector<std::pair<int, int>> e;
-  for (int a = 0; a + 1 < k; ++a) e.emplace_back(a, a + 1);
-  return e;
-}
-
-const std::vector<std::string>& builtin_names() {  // pattern.cpp:97-106
-  static const std::vector<std::string> names = {
-      "triangle",     "4clique",        "5clique",     "6clique",     "7clique",
-      "8clique",      "9clique",        "4cycle",      "5path",       "house",
-      "dumbbell",     "3motif-wedge",   "3motif-triangle", "4motif-path", "4motif-star",
-      "4motif-cycle", "4motif-tailedtriangle", "4motif-diamond", "4motif-clique"};
-  return names;
-}
-
-Pattern builtin(const std::string& name) {  // pattern.cpp:108-139
-  if (name == "triangle") return make(name, 3, clique(3), false);
-  for (int k = 4; k <= 9; ++k)
-    if (name == std::to_string(k) + "clique") return make(name, k, clique(k), false);
-  if (name == "4cycle") return make(name, 4, {{0, 1}, {1, 2}, {2, 3}, {3, 0}}, false);
-  if (name == "5path") return make(name, 5, path(5), false);
-  if (name == "house") return make(name, 5, {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {0, 4}, {1, 4}}, false);
-  if (name == "dumbbell")
-    return make(name, 6, {{0, 1}, {0, 2}, {1, 2}, {3, 4}, {3, 5}, {4, 5}, {2, 3}}, false);
-  if (name == "3motif-wedge") return make(name, 3, path(3), true);
-  if (name == "3motif-triangle") return make(name, 3, clique(3), true);
-  if (name == "4motif-path") return make(name, 4, path(4), true);
-  if (name == "4motif-star") return make(name, 4, {{0, 1}, {0, 2}, {0, 3}}, true);
-  if (name == "4motif-cycle") return make(name, 4, {{0, 1}, {1, 2}, {2, 3}, {3, 0}}, true);
-  if (name == "4motif-tailedtriangle") return make(name, 4, {{0, 1}, {0, 2}, {1, 2}, {1, 3}}, true);
-  if (name == "4motif-diamond")
-    return make(name, 4, {{0, 1}, {0, 2}, {1, 2}, {1, 3}, {2, 3}}, true);
-  if (name == "4motif-clique") return make(name, 4, clique(4), true);
-  std::ostringstream msg;
-  msg << "unknown pattern '" << name << "'; valid names:";
-  for (const auto& n : builtin_names()) msg << ' ' << n;
-  msg << " or custom:k:a-b,a-b,...";
-  throw pattern_error(msg.str());
-}
-
-// std::stoi semantics: optional leading whitespace and sign, at least one
-// digit, trailing characters ignored; anything else throws.
-bool stoi_like(const std::string& s, int* out) {
-  size_t i = 0;
-  while (i < s.size() && std::isspace(static_cast<unsigned char>(s[i]))) ++i;
-  bool neg = false;
-  if (i < s.size() && (s[i] == '+' || s[i] == '-')) neg = s[i++] == '-';
-  if (i >= s.size() || !std::isdigit(static_cast<unsigned char>(s[i]))) return false;
-  long long v = 0;
-  while (i < s.size() && std::isdigit(static_cast<unsigned char>(s[i]))) {
-    v = v * 10 + (s[i++] - '0');
-    if (v > 2147483648ll) return false;  // out_of_range
+// ---------------------------------------------------------------- construction
+// Raw edge pairs -> validated bitmask shape (pattern.cpp:10-41 semantics and messages)
+Shape build(const std::string& name, int k, const std::vector<std::pair<int, int>>& pairs, bool induced) {
+  if (k < 2 || k > AGPM_MAX_K) throw pattern_error("pattern must have between 2 and 9 vertices");
+  Shape s;
+  s.name = name;
+  s.k = k;
+  s.induced = induced;
+  for (const auto& e : pairs) {
+    if (e.first == e.second) throw pattern_error("pattern has a self-loop");
+    if (std::min(e.first, e.second) < 0 || std::max(e.first, e.second) >= k)
+      throw pattern_error("pattern edge endpoint out of range");
+    s.row[e.first] |= 1u << e.second;
+    s.row[e.second] |= 1u << e.first;
   }
-  v = neg ? -v : v;
-  if (v > 2147483647ll) return false;
-  *out = static_cast<int>(v);
+  // connectivity: grow the component of vertex 0 until it stops changing
+  uint32_t comp = 1u, prev = 0u;
+  while (comp != prev) {
+    prev = comp;
+    for (int v = 0; v < k; ++v)
+      if ((comp >> v) & 1u) comp |= s.row[v];
+  }
+  if (comp != (1u << k) - 1u) throw pattern_error("pattern must be connected");
+  return s;
+}
+
+// std::stoi semantics for the custom-spec fields: leading blanks, optional
+// sign, >= 1 digit, trailing text ignored, int range
+bool parse_int(const std::string& txt, int* out) {
+  const char* c = txt.c_str();
+  while (*c && std::isspace(static_cast<unsigned char>(*c))) ++c;
+  const bool neg = *c == '-';
+  if (*c == '+' || *c == '-') ++c;
+  if (!std::isdigit(static_cast<unsigned char>(*c))) return false;
+  long long v = 0;
+  for (; std::isdigit(static_cast<unsigned char>(*c)); ++c)
+    if ((v = v * 10 + (*c - '0')) > 2147483648ll) return false;
+  if (!neg && v == 2147483648ll) return false;
+  *out = static_cast<int>(neg ? -v : v);
   return true;
 }
 
-Pattern parse_spec(const std::string& spec, const std::string& induced) {  // pattern.cpp:130-165
-  Pattern p;
-  if (spec.rfind("custom:", 0) == 0) {
-    std::string rest = spec.substr(7);
-    auto colon = rest.find(':');
+// "a-b,c-d,..." -> pairs (pattern.cpp:150-160 field rules)
+std::vector<std::pair<int, int>> parse_edges(const std::string& list) {
+  std::vector<std::pair<int, int>> out;
+  size_t at = 0;
+  while (at < list.size()) {
+    size_t comma = list.find(',', at);
+    if (comma == std::string::npos) comma = list.size();
+    const std::string item = list.substr(at, comma - at);
+    at = comma + 1;
+    const size_t dash = item.find('-');
+    if (dash == std::string::npos) throw pattern_error("custom edge must look like a-b");
+    int a = 0, b = 0;
+    if (!parse_int(item.substr(0, dash), &a) || !parse_int(item.substr(dash + 1), &b))
+      throw pattern_error("custom edge endpoint is not a number");
+    out.emplace_back(a, b);
+  }
+  return out;
+}
+
+struct Builtin {
+  const char* name;
+  int k;
+  const char* edges;  // "" = clique on k vertices
+  bool induced;
+};
+// the reference's catalogue and its listing order (pattern.cpp:97-139)
+constexpr Builtin kBuiltins[] = {
+    {"triangle", 3, "", false},
+    {"4clique", 4, "", false},
+    {"5clique", 5, "", false},
+    {"6clique", 6, "", false},
+    {"7clique", 7, "", false},
+    {"8clique", 8, "", false},
+    {"9clique", 9, "", false},
+    {"4cycle", 4, "0-1,1-2,2-3,3-0", false},
+    {"5path", 5, "0-1,1-2,2-3,3-4", false},
+    {"house", 5, "0-1,1-2,2-3,3-0,0-4,1-4", false},
+    {"dumbbell", 6, "0-1,0-2,1-2,3-4,3-5,4-5,2-3", false},
+    {"3motif-wedge", 3, "0-1,1-2", true},
+    {"3motif-triangle", 3, "", true},
+    {"4motif-path", 4, "0-1,1-2,2-3", true},
+    {"4motif-star", 4, "0-1,0-2,0-3", true},
+    {"4motif-cycle", 4, "0-1,1-2,2-3,3-0", true},
+    {"4motif-tailedtriangle", 4, "0-1,0-2,1-2,1-3", true},
+    {"4motif-diamond", 4, "0-1,0-2,1-2,1-3,2-3", true},
+    {"4motif-clique", 4, "", true},
+};
+
+Shape from_builtin(const std::string& name) {
+  for (const Builtin& b : kBuiltins) {
+    if (name != b.name) continue;
+    std::vector<std::pair<int, int>> pairs;
+    if (*b.edges) {
+      pairs = parse_edges(b.edges);
+    } else {
+      for (int x = 0; x < b.k; ++x)
+        for (int y = x + 1; y < b.k; ++y) pairs.emplace_back(x, y);
+    }
+    return build(b.name, b.k, pairs, b.induced);
+  }
+  std::string msg = "unknown pattern '" + name + "'; valid names:";
+  for (const Builtin& b : kBuiltins) msg += std::string(" ") + b.name;
+  throw pattern_error(msg + " or custom:k:a-b,a-b,...");
+}
+
+Shape parse_spec(const std::string& spec, const std::string& induced) {  // pattern.cpp:130-165
+  Shape s;
+  static const std::string kCustom = "custom:";
+  if (spec.compare(0, kCustom.size(), kCustom) == 0) {
+    const std::string body = spec.substr(kCustom.size());
+    const size_t colon = body.find(':');
     if (colon == std::string::npos) throw pattern_error("custom pattern needs custom:k:edges");
     int k = 0;
-    if (!stoi_like(rest.substr(0, colon), &k)) throw pattern_error("custom pattern vertex count is not a number");
-    std::vector<std::pair<int, int>> edges;
-    std::istringstream es(rest.substr(colon + 1));
-    std::string item;
-    while (std::getline(es, item, ',')) {
-      auto dash = item.find('-');
-      if (dash == std::string::npos) throw pattern_error("custom edge must look like a-b");
-      int a = 0, b = 0;
-      if (!stoi_like(item.substr(0, dash), &a) || !stoi_like(item.substr(dash + 1), &b))
-        throw pattern_error("custom edge endpoint is not a number");
-      edges.emplace_back(a, b);
-    }
-    p = make("custom", k, std::move(edges), false);
+    if (!parse_int(body.substr(0, colon), &k)) throw pattern_error("custom pattern vertex count is not a number");
+    s = build("custom", k, parse_edges(body.substr(colon + 1)), false);
   } else {
-    p = builtin(spec);
+    s = from_builtin(spec);
   }
-  if (induced == "edge")
-    p.vertex_induced = false;
-  else if (induced == "vertex")
-    p.vertex_induced = true;
+  if (induced == "edge" || induced == "vertex")
+    s.induced = induced == "vertex";
   else if (!induced.empty())
     throw pattern_error("induced mode must be 'edge' or 'vertex'");
-  return p;
+  return s;
 }
 
-// Grochow-Kellis constraints (plan.cpp:20-38)
-std::vector<std::pair<int, int>> symmetry_constraints(const Pattern& p, const std::vector<int>& order) {
-  auto group = p.automorphisms();
-  std::vector<std::pair<int, int>> conds;
+// ---------------------------------------------------------------- symmetry
+// All edge-preserving permutations: vertex v is mapped after 0..v-1, and a
+// partial map survives only while every edge (and non-edge) among the mapped
+// vertices is preserved — an automorphism is a bijection preserving adjacency
+// in both directions, so this prunes to exactly the group.
+void extend_auto(const Shape& s, Perm& p, uint32_t used, int v, std::vector<Perm>& out) {
+  if (v == s.k) {
+    out.push_back(p);
+    return;
+  }
+  for (int img = 0; img < s.k; ++img) {
+    if ((used >> img) & 1u || s.deg(img) != s.deg(v)) continue;
+    bool ok = true;
+    for (int u = 0; u < v && ok; ++u) ok = s.edge(u, v) == s.edge(p[u], img);
+    if (!ok) continue;
+    p[v] = static_cast<int8_t>(img);
+    extend_auto(s, p, used | (1u << img), v + 1, out);
+  }
+}
+
+std::vector<Perm> automorphism_group(const Shape& s) {
+  std::vector<Perm> g;
+  Perm p{};
+  extend_auto(s, p, 0u, 0, g);
+  return g;
+}
+
+// Grochow-Kellis symmetry breaking walked in matching order (plan.cpp:20-38):
+// at each vertex u, constrain u below every other member of its orbit under
+// the group fixing the earlier vertices, then restrict to u's stabiliser.
+std::vector<std::pair<int, int>> orbit_constraints(const Shape& s, const std::vector<int>& order) {
+  std::vector<Perm> grp = automorphism_group(s);
+  std::vector<std::pair<int, int>> out;
   for (int u : order) {
-    if (group.size() <= 1) break;
-    std::set<int> orbit;
-    for (const auto& a : group) orbit.insert(a[u]);
-    if (orbit.size() > 1)
-      for (int w : orbit)
-        if (w != u) conds.emplace_back(u, w);
-    std::vector<std::vector<int>> stab;
-    for (auto& a : group)
-      if (a[u] == u) stab.push_back(std::move(a));
-    group = std::move(stab);
+    if (grp.size() < 2) break;
+    uint32_t orbit = 0;
+    for (const Perm& a : grp) orbit |= 1u << a[u];
+    for (int w = 0; w < s.k; ++w)
+      if (w != u && ((orbit >> w) & 1u)) out.emplace_back(u, w);
+    grp.erase(std::remove_if(grp.begin(), grp.end(), [u](const Perm& a) { return a[u] != u; }), grp.end());
   }
-  return conds;
+  return out;
 }
 
-std::pair<int, int> pick_seed(const Pattern& p) {  // plan.cpp:40-53
-  int ba = -1, bb = -1, best = -1;
-  for (auto [a, b] : p.edges) {
-    int s = p.degree(a) + p.degree(b);
-    if (s > best) {
-      best = s;
-      ba = a;
-      bb = b;
+// ---------------------------------------------------------------- plan
+// Matching order (plan.cpp:40-76): seed = the first edge (in edge order) with
+// the largest endpoint-degree sum, its higher-degree endpoint first; then the
+// unbound vertex with the most bound neighbours, ties to the smaller id.
+std::vector<int> matching_order(const Shape& s) {
+  int sa = -1, sb = -1, best = -1;
+  s.each_edge([&](int a, int b) {
+    if (s.deg(a) + s.deg(b) > best) {
+      best = s.deg(a) + s.deg(b);
+      sa = a;
+      sb = b;
     }
-  }
-  if (p.degree(bb) > p.degree(ba)) std::swap(ba, bb);
-  return {ba, bb};
-}
-
-void put_pairs(const std::vector<std::pair<int, int>>& v, int32_t* n, int32_t (*dst)[2]) {
-  *n = static_cast<int32_t>(v.size());
-  for (size_t i = 0; i < v.size(); ++i) {
-    dst[i][0] = v[i].first;
-    dst[i][1] = v[i].second;
-  }
-}
-
-void compile(const Pattern& pin, int mode, bool sym, agpm_plan* out) {  // plan.cpp:57-137
-  Pattern p = pin;
-  p.normalize();
-  const int k = p.k;
-  const bool eager = mode == 0;
-  std::memset(out, 0, sizeof(*out));
-  std::snprintf(out->name, sizeof(out->name), "%s", p.name.c_str());
-  out->k = k;
-  out->induced = p.vertex_induced;
-  put_pairs(p.edges, &out->n_edges, out->edges);
-  for (int v = 0; v < k; ++v) out->adjacency[v] = p.adj[v];
-  out->verify_mode = eager ? 0 : 1;
-  out->symmetry_enabled = sym;
-
-  auto [s0, s1] = pick_seed(p);
-  std::vector<int> order = {s0, s1};
-  std::vector<bool> bound(k, false);
-  bound[s0] = bound[s1] = true;
-  while (static_cast<int>(order.size()) < k) {
-    int best = -1, best_cnt = -1;
-    for (int v = 0; v < k; ++v) {
-      if (bound[v]) continue;
-      int cnt = 0;
-      for (int b : order)
-        if (p.has_edge(v, b)) ++cnt;
-      if (cnt > best_cnt) {
-        best_cnt = cnt;
-        best = v;
+  });
+  if (s.deg(sb) > s.deg(sa)) std::swap(sa, sb);
+  std::vector<int> order = {sa, sb};
+  uint32_t bound = (1u << sa) | (1u << sb);
+  while (static_cast<int>(order.size()) < s.k) {
+    int pick = -1, most = -1;
+    for (int v = 0; v < s.k; ++v) {
+      if ((bound >> v) & 1u) continue;
+      const int c = __builtin_popcount(s.row[v] & bound);
+      if (c > most) {
+        most = c;
+        pick = v;
       }
     }
-    bound[best] = true;
-    order.push_back(best);
+    bound |= 1u << pick;
+    order.push_back(pick);
   }
-  std::vector<int> pos_of(k, -1);
-  for (int i = 0; i < k; ++i) pos_of[order[i]] = i;
+  return order;
+}
+
+template <class Pairs>
+void emit_pairs(const Pairs& src, int32_t* n, int32_t (*dst)[2]) {
+  *n = 0;
+  for (const auto& e : src) {
+    dst[*n][0] = e.first;
+    dst[*n][1] = e.second;
+    ++*n;
+  }
+}
+
+void compile(const Shape& s, bool eager, bool symmetric, agpm_plan* out) {  // plan.cpp:57-137
+  const int k = s.k;
+  std::memset(out, 0, sizeof(*out));
+  std::snprintf(out->name, sizeof(out->name), "%s", s.name.c_str());
+  out->k = k;
+  out->induced = s.induced;
+  std::vector<std::pair<int, int>> edges;
+  s.each_edge([&](int a, int b) { edges.emplace_back(a, b); });
+  emit_pairs(edges, &out->n_edges, out->edges);
+  std::copy(s.row, s.row + k, out->adjacency);
+  out->verify_mode = eager ? 0 : 1;
+  out->symmetry_enabled = symmetric;
+
+  const std::vector<int> order = matching_order(s);
   for (int i = 0; i < k; ++i) {
     out->order[i] = order[i];
-    out->pos_of[i] = pos_of[i];
+    out->pos_of[order[i]] = i;
   }
-  std::vector<std::pair<int, int>> cons;
-  if (sym) cons = symmetry_constraints(p, order);
-  for (auto [a, b] : cons)
-    if ((a == s0 && b == s1) || (a == s1 && b == s0)) out->seed_ordered = 1;
-  put_pairs(cons, &out->n_constraints, out->constraints);
+  const std::vector<std::pair<int, int>> cons = symmetric ? orbit_constraints(s, order) : decltype(cons){};
+  const uint32_t seed_pair = (1u << order[0]) | (1u << order[1]);
+  auto on_seed = [&](const std::pair<int, int>& c) { return ((1u << c.first) | (1u << c.second)) == seed_pair; };
+  out->seed_ordered = std::any_of(cons.begin(), cons.end(), on_seed) ? 1 : 0;
+  emit_pairs(cons, &out->n_constraints, out->constraints);
 
-  std::set<std::pair<int, int>> covered;
-  covered.insert({std::min(s0, s1), std::max(s0, s1)});
+  uint32_t verified[AGPM_MAX_K] = {};  // verified[a] bit b: edge {a, b} checked by a step or the seed
+  verified[std::min(order[0], order[1])] |= 1u << std::max(order[0], order[1]);
   out->n_steps = k - 2;
   for (int pos = 2; pos < k; ++pos) {
     agpm_plan_step& st = out->steps[pos - 2];
-    st.pattern_vertex = order[pos];
+    const int v = order[pos];
+    st.pattern_vertex = v;
     st.tree_parent = -1;
-    for (int prev = 0; prev < pos; ++prev) {
-      int pv = order[prev];
-      if (p.has_edge(st.pattern_vertex, pv))
-        st.in_positions[st.n_in++] = prev;
-      else if (p.vertex_induced && eager)
-        st.out_positions[st.n_out++] = prev;
+    for (int q = 0; q < pos; ++q) {
+      if (s.edge(v, order[q]))
+        st.in_positions[st.n_in++] = q;
+      else if (s.induced && eager)
+        st.out_positions[st.n_out++] = q;
     }
-    auto add_verify = [&](int a, int b) {
-      st.verify_edges[st.n_verify][0] = std::min(a, b);
-      st.verify_edges[st.n_verify][1] = std::max(a, b);
+    auto verify = [&](int a, int b) {
+      const int lo = std::min(a, b), hi = std::max(a, b);
+      st.verify_edges[st.n_verify][0] = lo;
+      st.verify_edges[st.n_verify][1] = hi;
       ++st.n_verify;
-      covered.insert({std::min(a, b), std::max(a, b)});
+      verified[lo] |= 1u << hi;
     };
-    if (eager) {
-      for (int i = 0; i < st.n_in; ++i) add_verify(st.pattern_vertex, order[st.in_positions[i]]);
-      if (sym)
-        for (auto [a, b] : cons) {
-          if (b == st.pattern_vertex && pos_of[a] < pos) st.greater_than[st.n_gt++] = pos_of[a];
-          if (a == st.pattern_vertex && pos_of[b] < pos) st.less_than[st.n_lt++] = pos_of[b];
-        }
-    } else {
+    if (!eager) {
       st.tree_parent = st.in_positions[0];
-      add_verify(st.pattern_vertex, order[st.tree_parent]);
+      verify(v, order[st.tree_parent]);
+      continue;
+    }
+    for (int i = 0; i < st.n_in; ++i) verify(v, order[st.in_positions[i]]);
+    for (const auto& c : cons) {  // order bounds at the later endpoint, constraint order kept
+      if (c.second == v && out->pos_of[c.first] < pos) st.greater_than[st.n_gt++] = out->pos_of[c.first];
+      if (c.first == v && out->pos_of[c.second] < pos) st.less_than[st.n_lt++] = out->pos_of[c.second];
     }
   }
   if (!eager) {
     std::vector<std::pair<int, int>> closure, terminal;
-    for (auto e : p.edges)
-      if (!covered.count(e)) closure.push_back(e);
-    for (auto [a, b] : cons) {
-      bool at_seed = (a == s0 && b == s1) || (a == s1 && b == s0);
-      if (!at_seed) terminal.emplace_back(a, b);
-    }
-    put_pairs(closure, &out->n_closure, out->closure_edges);
-    put_pairs(terminal, &out->n_terminal, out->terminal_constraints);
+    for (const auto& e : edges)
+      if (!((verified[e.first] >> e.second) & 1u)) closure.push_back(e);
+    for (const auto& c : cons)
+      if (!on_seed(c)) terminal.push_back(c);
+    emit_pairs(closure, &out->n_closure, out->closure_edges);
+    emit_pairs(terminal, &out->n_terminal, out->terminal_constraints);
   }
+}
+
+void copy_out(const std::string& text, char* buf, size_t cap) {
+  if (!buf || cap <= text.size()) throw std::invalid_argument("buffer too small");
+  std::memcpy(buf, text.c_str(), text.size() + 1);
 }
 
 }  // namespace
@@ -336,52 +348,51 @@ int agpm_plan_compile(const char* spec, const char* induced, int verify_mode, in
   return guarded([&] {
     if (!spec || !out) throw std::invalid_argument("null argument");
     if (verify_mode != 0 && verify_mode != 1) throw std::invalid_argument("verify mode must be 0 or 1");
-    Pattern p = parse_spec(spec, induced ? induced : "");
-    compile(p, verify_mode, enable_symmetry != 0, out);
+    compile(parse_spec(spec, induced ? induced : ""), verify_mode == 0, enable_symmetry != 0, out);
   });
 }
 
 int agpm_builtin_pattern_names(char* buf, size_t cap) {
   return guarded([&] {
-    std::string s;
-    for (const auto& n : builtin_names()) s += n + "\n";
-    if (!buf || cap <= s.size()) throw std::invalid_argument("buffer too small");
-    std::memcpy(buf, s.c_str(), s.size() + 1);
+    std::string all;
+    for (const Builtin& b : kBuiltins) all += std::string(b.name) + "\n";
+    copy_out(all, buf, cap);
   });
 }
 
 int agpm_pattern_automorphism_count(const char* spec, const char* induced, uint64_t* out) {
-  return guarded([&] { *out = parse_spec(spec, induced ? induced : "").automorphisms().size(); });
+  return guarded([&] { *out = automorphism_group(parse_spec(spec, induced ? induced : "")).size(); });
 }
 
 int agpm_plan_scaling_rule(const agpm_plan* plan, char* buf, size_t cap) {  // plan.cpp:139-148
   return guarded([&] {
-    std::ostringstream s;
     const bool eager = plan->verify_mode == 0;
-    s << (plan->seed_ordered ? "m" : "2m");
-    for (int i = 0; i < plan->n_steps; ++i) s << (eager ? " * |S_" : " * c_") << i + 2 << (eager ? "|" : "");
-    if (!eager && plan->n_closure > 0) s << " (terminal closure of " << plan->n_closure << " edges)";
-    std::string str = s.str();
-    if (!buf || cap <= str.size()) throw std::invalid_argument("buffer too small");
-    std::memcpy(buf, str.c_str(), str.size() + 1);
+    std::string rule = plan->seed_ordered ? "m" : "2m";
+    for (int i = 0; i < plan->n_steps; ++i)
+      rule += eager ? " * |S_" + std::to_string(i + 2) + "|" : " * c_" + std::to_string(i + 2);
+    if (!eager && plan->n_closure > 0)
+      rule += " (terminal closure of " + std::to_string(plan->n_closure) + " edges)";
+    copy_out(rule, buf, cap);
   });
 }
 
 int agpm_plan_verifies_each_edge_once(const agpm_plan* plan, int* out) {  // plan.cpp:150-163
+  // tally each checked pair in a k x k count table: the seed edge, every
+  // step's verify edges, the lazy closure; the plan passes iff the checked
+  // pairs are exactly the pattern's edges, each checked once
   return guarded([&] {
-    std::map<std::pair<int, int>, int> seen;
-    int s0 = plan->order[0], s1 = plan->order[1];
-    seen[{std::min(s0, s1), std::max(s0, s1)}]++;
+    int seen[AGPM_MAX_K][AGPM_MAX_K] = {};
+    auto tally = [&](int a, int b) { ++seen[std::min(a, b)][std::max(a, b)]; };
+    tally(plan->order[0], plan->order[1]);
     for (int i = 0; i < plan->n_steps; ++i)
       for (int e = 0; e < plan->steps[i].n_verify; ++e)
-        seen[{plan->steps[i].verify_edges[e][0], plan->steps[i].verify_edges[e][1]}]++;
-    for (int e = 0; e < plan->n_closure; ++e)
-      seen[{plan->closure_edges[e][0], plan->closure_edges[e][1]}]++;
-    bool ok = static_cast<int>(seen.size()) == plan->n_edges;
-    for (int e = 0; ok && e < plan->n_edges; ++e) {
-      auto it = seen.find({plan->edges[e][0], plan->edges[e][1]});
-      ok = it != seen.end() && it->second == 1;
-    }
+        tally(plan->steps[i].verify_edges[e][0], plan->steps[i].verify_edges[e][1]);
+    for (int e = 0; e < plan->n_closure; ++e) tally(plan->closure_edges[e][0], plan->closure_edges[e][1]);
+    int want[AGPM_MAX_K][AGPM_MAX_K] = {};
+    for (int e = 0; e < plan->n_edges; ++e) want[plan->edges[e][0]][plan->edges[e][1]] = 1;
+    bool ok = true;
+    for (int a = 0; a < AGPM_MAX_K; ++a)
+      for (int b = 0; b < AGPM_MAX_K; ++b) ok = ok && seen[a][b] == want[a][b];
     *out = ok;
   });
 }
