@@ -375,8 +375,9 @@ int agpm_count_hybrid(const agpm_host_graph* hg, agpm_graph* g, const agpm_plan*
  * Builder-defined (no reference implementation). On a
  * degree-relabelled view: V_s = {deg < tau} = ids [0, tau_id); C_sparse =
  * matches touching V_s, exact; C_dense on G[V_d] by dense_method 0 = online NS
- * (eps, delta, max_samples), 1 = mean of `repeats` colourings with `colors`
- * colours, 2 = exact. estimate = C_sparse + C_dense. On an oriented clique DAG
+ * (eps, delta, max_samples), 1 = colour GS with `colors` colours repeated to
+ * eps@delta (agpm_gs_online, at most `repeats` colourings; dense_ns holds that
+ * run: windows = colourings), 2 = exact. estimate = C_sparse + C_dense. On an oriented clique DAG
  * tau_degree is taken as the id threshold tau_id itself. */
 typedef struct agpm_region_result {
   uint32_t tau_id;

@@ -81,7 +81,7 @@ uint64_t count_matches_through_edge_view(const HostView& g, const agpm_plan& p, 
   const int k = p.k;
   uint64_t maps = 0;
   std::vector<uint32_t> image(k, 0);
-  std::vector<bool> used(g.n, false);
+  std::vector<uint8_t> used(g.n, 0);
   std::vector<int> ext_order;
   auto nb = [&](uint32_t x) { return g.nbr + g.begin[x]; };
   std::function<uint64_t(size_t, uint32_t)> extend = [&](size_t depth, uint32_t assigned) -> uint64_t {
@@ -158,6 +158,8 @@ uint64_t estimate_gamma_view(const HostView& g, const agpm_plan& p, uint64_t pro
   for (uint32_t x = 0; x < g.n; ++x) prefix[x + 1] = prefix[x] + g.degree(x);
   CounterRng rng(seed, 0x67616d6dull);  // "gamm"
   uint64_t best = 0;
+  // one budget across the probes: a lower bound either way, so running out
+  // mid-probe just stops with the maximum seen so far
   for (uint64_t i = 0; i < probe_edges && work_budget > 0; ++i) {
     const uint64_t idx = rng.next_below(prefix.back());
     const auto it = std::upper_bound(prefix.begin(), prefix.end(), idx);

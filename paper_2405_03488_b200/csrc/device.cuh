@@ -83,6 +83,11 @@ struct DeviceGuard {
   DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
+// the plan is the edge-induced eager 4-cycle (k = 4, 4 edges, every vertex of degree 2)
+bool plan_is_plain_4cycle(const agpm_plan* p);
+// 4-cycles whose minimum vertex is < tau_id on a plain, symmetric, degree-relabelled
+// view (cycle4_sparse.cu): the region split's C_sparse for the 4-cycle plan
+unsigned long long cycle4_sparse_count(agpm_graph* g, uint32_t tau_id, cudaStream_t s);
 }  // namespace agpm_b200
 
 // C-ABI opaque handle
@@ -122,4 +127,9 @@ void ensure_twin_arcs(agpm_graph* g, cudaStream_t s);
 // first vertex is below it, shard/nshards keep every nshards-th 32-arc chunk
 unsigned long long exact_count_device(const agpm_graph* g, const agpm_plan* plan, cudaStream_t s,
                                       uint32_t root_limit = 0xffffffffu, uint32_t shard = 0, uint32_t nshards = 1);
+// the plan is the edge-induced eager 4-cycle (k = 4, 4 edges, every vertex of degree 2)
+bool plan_is_plain_4cycle(const agpm_plan* p);
+// 4-cycles whose minimum vertex is < tau_id on a plain, symmetric, degree-relabelled
+// view (cycle4_sparse.cu): the region split's C_sparse for the 4-cycle plan
+unsigned long long cycle4_sparse_count(agpm_graph* g, uint32_t tau_id, cudaStream_t s);
 }  // namespace agpm_b200

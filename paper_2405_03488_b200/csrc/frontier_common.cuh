@@ -14,8 +14,13 @@ constexpr unsigned long long kFrontierCap = 1ull << 24;  // samples per pass
 constexpr uint32_t NO_DRV = 0xffffffffu;
 
 // Per-sample intersection job; other-list slots are indexed by matching position.
+// Alignment: 16 B (vector loads in the frontier's global descriptor array) unless
+// the including sampler asks otherwise (the flat sampler keeps them in shared memory).
+#ifndef AGPM_DESC_ALIGN
+#define AGPM_DESC_ALIGN 16
+#endif
 template <int K>
-struct __align__(16) IsectDesc {
+struct __align__(AGPM_DESC_ALIGN) IsectDesc {
   const uint32_t* drv;                // driver list (adjacency range or compacted survivors)
   unsigned long long start[K - 1];    // other lists: in-lists restricted, out-lists whole
   uint32_t len[K - 1];

@@ -3,6 +3,10 @@
 #include <cstdlib>
 #include <stdexcept>
 
+#ifndef AGPM_FLAT_DESC_ALIGN
+#define AGPM_FLAT_DESC_ALIGN 16
+#endif
+#define AGPM_DESC_ALIGN AGPM_FLAT_DESC_ALIGN
 #include "frontier_common.cuh"
 
 namespace agpm_b200 {
@@ -343,6 +347,9 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
   auto kern = fr_flat_kernel<K, AGPM_FLAT_U, kMinB, R>;
   static int occ = -1;
   if (occ < 0) {
+#ifdef AGPM_FLAT_CARVEOUT
+    AGPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, AGPM_FLAT_CARVEOUT));
+#endif
     int o = 0;
     AGPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kFlatThreads, 0));
     occ = std::max(o, 1);

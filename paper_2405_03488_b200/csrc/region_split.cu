@@ -193,7 +193,10 @@ int agpm_region_split(agpm_graph* g, const agpm_plan* plan, uint32_t tau_degree,
     agpm_graph* dense = induced_suffix_device(g, tau_id, s);
     out->dense_edges = dense->edge_count;
     try {
-      if (out->rooted) {
+      if (out->rooted && plan_is_plain_4cycle(plan) && g->plain && !g->oriented) {
+        // 4-cycles: pair aggregation instead of the wedge-by-wedge DFS through hubs
+        out->c_sparse = cycle4_sparse_count(g, tau_id, s);
+      } else if (out->rooted) {
         out->c_sparse = exact_count_device(g, plan, s, tau_id);
       } else {
         out->c_sparse = exact_count_device(g, plan, s, 0xffffffffu) - exact_count_device(dense, plan, s, 0xffffffffu);
@@ -206,20 +209,15 @@ int agpm_region_split(agpm_graph* g, const agpm_plan* plan, uint32_t tau_degree,
       } else if (dense_method == 2) {
         out->c_dense = static_cast<double>(exact_count_device(dense, plan, s, 0xffffffffu));
         out->dense_exact = 1;
-      } else if (dense_method == 1) {  // repeated colourings: each is an unbiased coarse sample
-        const uint32_t r = std::max<uint32_t>(1, repeats);
-        double sum = 0.0, sq = 0.0;
-        for (uint32_t i = 0; i < r; ++i) {
-          agpm_gs_result gr{};
-          if (agpm_gs_estimate(dense, plan, 1, 1.0, colors, derive_key(seed, i, 0), &gr, s) != AGPM_OK)
-            throw std::runtime_error(agpm_last_error());
-          sum += gr.estimate;
-          sq += gr.estimate * gr.estimate;
-        }
-        out->c_dense = sum / r;
-        agpm_accumulator acc{r, r, sum, sq};
-        agpm_report rep{};
-        if (agpm_predicted_error(&acc, delta, &rep) == AGPM_OK) out->dense_epsilon_hat = rep.epsilon_hat;
+      } else if (dense_method == 1) {
+        // repeated colourings, each an unbiased coarse sample c^(k-1) x raw
+        // (gs_engine.cpp:42-75), run under the online detector to eps@delta
+        // (Appendix C.2) with `repeats` as the cap on colourings
+        if (agpm_gs_online(dense, plan, colors, eps, delta, std::max<uint32_t>(2, repeats), seed, &out->dense_ns, s) !=
+            AGPM_OK)
+          throw std::runtime_error(agpm_last_error());
+        out->c_dense = out->dense_ns.report.mu;
+        out->dense_epsilon_hat = out->dense_ns.report.epsilon_hat;
       } else {
         agpm_online_policy pol{1000, max_samples ? max_samples : 1000000000ull, 0};
         if (agpm_ns_online(dense, plan, eps, delta, &pol, seed, &out->dense_ns, s) != AGPM_OK)

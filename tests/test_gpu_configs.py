@@ -8,8 +8,10 @@ config 2  4-clique, RMAT-20 ef16 relabelled, run_ns_online to 1 %@95 %: the devi
           of the exact count.
 config 4  needle: ER n = 2^22, avg degree 8, 1000 planted 5-cliques — the
           region split finds every planted clique exactly.
-(config 3 / 5 sizes are exercised by bench.py and the parity suites at smaller
-scale; their exact counts are infeasible for the CPU oracle.)
+config 4  the colour-GS dense leg: with tau = 10 about a third of the planted
+          K5s lie entirely in the dense region, so c = 4 colourings repeated to
+          1 %@95 % estimate a real count there, checked against the exact count.
+(configs 3 / 5 at size: tests/test_gpu_scale.py.)
 """
 import pytest
 
@@ -58,3 +60,25 @@ def test_config4_needle(agpm):
     assert res.c_sparse + (int(res.c_dense) if res.dense_exact else 0) <= exact
     full = agpm.region_split(dg, plan, 16, dense="exact")
     assert full.estimate == exact
+
+
+@pytest.mark.slow
+def test_config4_gs_dense_leg(agpm):
+    """Config 4's c = 4 colour-GS leg on a dense region that holds planted K5s
+    (gs_engine.cpp:42-75 per colouring, the online detector over colourings):
+    sparse part exact, dense part within the error bound of the exact count."""
+    n = 1 << 22
+    g = agpm.er_fast(n, n * 4, seed=4, planted_k=5, planted_count=1000).relabel_by_degree()
+    dg = agpm.DeviceGraph(g)
+    plan = agpm.compile_plan("5clique")
+    exact = agpm.exact_count(dg, plan)
+    tau = 10  # planted vertices have degree ~ Poisson(8) + 4: many reach the dense region
+    ex = agpm.region_split(dg, plan, tau, dense="exact")
+    assert ex.estimate == exact
+    dense_truth = exact - ex.c_sparse
+    assert dense_truth >= 100  # a real population of K5s for GS to estimate
+    gs = agpm.region_split(dg, plan, tau, dense="gs", colors=4, eps=0.01, delta=0.05, repeats=200000, seed=11)
+    assert gs.c_sparse == ex.c_sparse
+    assert gs.dense_ns.report.converged and gs.dense_epsilon_hat <= 0.01
+    # 1 %@95 %: allow 3 eps (a ~1-in-10^3 event) so the test is not flaky
+    assert abs(gs.c_dense - dense_truth) <= 0.03 * dense_truth, (gs.c_dense, dense_truth, gs.dense_ns.windows)
