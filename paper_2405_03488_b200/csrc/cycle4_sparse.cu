@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kC4Threads) c4_direct_kernel(C4Args A) {
 }  // namespace
 
 bool plan_is_plain_4cycle(const agpm_plan* p) {
-  if (p->k != 4 || p->n_edges != 4 || p->induced || p->verify_mode != 0) return false;
+  if (p->k != 4 || p->n_edges != 4 || p->induced || p->verify_mode != 0 || !p->symmetry_enabled) return false;
   for (int v = 0; v < 4; ++v)
     if (__builtin_popcount(p->adjacency[v]) != 2) return false;
   return true;
