@@ -16,6 +16,13 @@ constexpr uint32_t NO_DRV = 0xffffffffu;
 // Per-sample intersection job; other-list slots are indexed by matching position.
 // Alignment: 16 B (vector loads in the frontier's global descriptor array) unless
 // the including sampler asks otherwise (the flat sampler keeps them in shared memory).
+// Twin hints for picked vertices (DevPlan::twin_hint) in the frontier phases: off.
+// Measured per 2^24 4-cycle samples (the plan they target): RMAT-20 8.74 -> 8.95 ms,
+// RMAT-22 13.39 -> 13.62 ms with them — N(v2)'s superset range already keeps it
+// off the driver, so the exact range only costs the twin gather.
+#ifndef AGPM_TWIN_HINT_SINGLE
+#define AGPM_TWIN_HINT_SINGLE 0
+#endif
 #ifndef AGPM_DESC_ALIGN
 #define AGPM_DESC_ALIGN 16
 #endif
@@ -316,13 +323,19 @@ __device__ int advance(const FrontierArgs& A, unsigned long long i, Sample<K, R>
       }
       S.alpha = __dmul_rn(S.alpha, (double)cnt);  // alpha *= |S_j| (ns_engine.cpp:39)
       const uint32_t pick = ldn(dptr, o);
+      uint32_t from = 0;
 #pragma unroll
       for (int q = 0; q < j; ++q)
         if (q == drv) {
           S.hbo[q] = drs + o + 1;
           S.hbl[q] = pick + 1;
+          from = S.bnd[q];
         }
       bind(S, j, pick);
+      if (AGPM_TWIN_HINT_SINGLE && p.twin_hint[s] && A.g.twin && drv >= 0) {  // position of v_drv in N(pick)
+        S.hbo[j] = __ldg(A.g.twin + (unsigned long long)(dptr - nbr) + o) + 1;
+        S.hbl[j] = from + 1;
+      }
       continue;
     }
     // multi-list step: hand the intersection to the word-parallel phase

@@ -27,6 +27,11 @@ struct DevPlan {
   unsigned short out_mask[AGPM_MAX_K - 2];
   unsigned short gt_mask[AGPM_MAX_K - 2];
   unsigned short lt_mask[AGPM_MAX_K - 2];
+  // step s: after picking v_j (j = s + 2) from the list of bound position q, a
+  // later step bounds N(v_j) by bnd[q] (e.g. the 4-cycle's S_3 = N(v0) ∩ N(v2)
+  // > v1, with v2 picked from N(v1)): the twin arc of the pick then gives
+  // lower_bound(bnd[q] + 1) in N(v_j) for free (core_bits.cu twin index)
+  unsigned char twin_hint[AGPM_MAX_K - 2];
   // lazy verification (VerifyMode::Lazy, walker.hpp:56-62 / 88-107), positions
   int lazy;
   unsigned char tree_parent[AGPM_MAX_K - 2];

@@ -165,6 +165,10 @@ DevPlan make_dev_plan(const agpm_graph* g, const agpm_plan* plan) {
       d.tree_parent[s] = (unsigned char)st.tree_parent;
     }
   }
+  for (int s = 0; s < d.n_steps; ++s)
+    for (int s2 = s + 1; s2 < d.n_steps; ++s2)
+      if (((d.in_mask[s2] >> (s + 2)) & 1u) && ((d.gt_mask[s2] | d.lt_mask[s2]) & d.in_mask[s]))
+        d.twin_hint[s] = 1;
   d.lazy = plan->verify_mode == 1;
   if (d.lazy) {  // pattern vertices -> positions (walker.hpp:88-107)
     auto pos = [&](int v) {

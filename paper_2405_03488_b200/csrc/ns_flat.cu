@@ -314,7 +314,15 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
                 S.hbl[q] = pick + 1;
               }
           }
+          uint32_t from = 0;
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if ((uint32_t)q == dpos) from = S.bnd[q];
           bind(S, j, pick);
+          if (A.p.twin_hint[pend] && A.g.twin && dpos != NO_DRV) {  // position of v_drv in N(pick)
+            S.hbo[j] = __ldg(A.g.twin + (unsigned long long)(my.drv - A.g.nbr) + o_pick) + 1;
+            S.hbl[j] = from + 1;
+          }
           pend = advance<K>(A, i, S, pend + 1, nullptr, 0, &my);
         }
       }

@@ -35,6 +35,9 @@
 #include <stdexcept>
 
 #include "frontier_common.cuh"
+#ifndef AGPM_TWIN_HINT_MULTI
+#define AGPM_TWIN_HINT_MULTI 0  // see AGPM_TWIN_HINT_SINGLE
+#endif
 
 namespace agpm_b200 {
 
@@ -263,6 +266,14 @@ __global__ void __launch_bounds__(256) fr_pick_kernel(const FrontierArgs A, int 
             }
         }
         bind(S, j, pick);
+        if (AGPM_TWIN_HINT_MULTI && A.p.twin_hint[s_step] && A.g.twin && dp->drv_pos != NO_DRV) {  // position of v_drv in N(pick)
+          uint32_t from = 0;
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if ((uint32_t)q == dp->drv_pos) from = S.bnd[q];
+          S.hbo[j] = __ldg(A.g.twin + (unsigned long long)(D - nbr) + o_pick) + 1;
+          S.hbl[j] = from + 1;
+        }
         alive = true;
         if (reuse_next) {
           step_bounds(A.p, s_step + 1, S, lo2, hi2);
