@@ -12,9 +12,9 @@ A.set_core_dim(core)
 graph = sys.argv[5] if len(sys.argv) > 5 else "rmat20"
 if graph == "er10k":  # config 1
     g = A.er_graph(10000, 20 / 9999, 1).relabel_by_degree()
-else:
-    g = A.rmat(int(graph[4:]), 16, seed=1).relabel_by_degree()
-dg = A.DeviceGraph(g)
+    dg = A.DeviceGraph(g)
+else:  # built on the device (== the host builder, tests/test_gpu_ingest.py)
+    dg = A.rmat_device(int(graph[4:]), 16, seed=1)
 plan = A.compile_plan(pattern)
 A.set_strategy(strategy)
 if os.environ.get("AGPM_RNG"):
