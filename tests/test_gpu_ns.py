@@ -258,9 +258,14 @@ def test_twin_arc_hints_same_samples(agpm, oracle, graphs, strat, pattern):
         dg = agpm.DeviceGraph(g)
         agpm.set_strategy(strat)
         try:
-            runs = [agpm.draw_samples(dg, plan, 5, 300, 5000) for _ in range(3)]
+            runs, sizes = [], []
+            for _ in range(3):
+                runs.append(agpm.draw_samples(dg, plan, 5, 300, 5000))
+                sizes.append(dg.info()["device_bytes"])
         finally:
             agpm.set_strategy("auto")
+        # the index really exists from the second launch on (4 B per arc), and only then
+        assert sizes[1] - sizes[0] == 4 * dg.info()["arcs"] and sizes[2] == sizes[1]
         ov, oh, ob = oracle.draw_records(off, nbr, g.edge_count, plan, 5, 300, 5000)
         for v, h, b in runs:
             np.testing.assert_array_equal(v, ov)
