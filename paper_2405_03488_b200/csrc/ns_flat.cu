@@ -320,8 +320,23 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
             if ((uint32_t)q == dpos) from = S.bnd[q];
           bind(S, j, pick);
           if (A.p.twin_hint[pend] && A.g.twin && dpos != NO_DRV) {  // position of v_drv in N(pick)
-            S.hbo[j] = __ldg(A.g.twin + (unsigned long long)(my.drv - A.g.nbr) + o_pick) + 1;
-            S.hbl[j] = from + 1;
+            const uint32_t tw = __ldg(A.g.twin + (unsigned long long)(my.drv - A.g.nbr) + o_pick) + 1;
+            // Placement: for K >= 4 the hint arrays are addressed with the runtime
+            // position j here, which puts them in local memory (an L1-resident
+            // stack) instead of competing for the 48 registers of the hot loop —
+            // measured per 2^24 samples: 4-clique 8.15 -> 7.75 ms, 5-clique 11.8 ->
+            // 10.6 ms; K = 3 keeps them in registers (triangle 5.13 vs 5.38 ms).
+            if constexpr (K >= 4) {
+              S.hbo[j] = tw;
+              S.hbl[j] = from + 1;
+            } else {
+#pragma unroll
+              for (int q = 2; q < K; ++q)
+                if (q == j) {
+                  S.hbo[q] = tw;
+                  S.hbl[q] = from + 1;
+                }
+            }
           }
           pend = advance<K>(A, i, S, pend + 1, nullptr, 0, &my);
         }
