@@ -366,7 +366,10 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
   // a cap costs. Measured per 2^24 samples on the config-2 graph: 4-clique 96
   // regs 14.2 ms, 64 regs 9.1, 56 regs 8.9, 48 regs 8.8, 40 regs 9.9; triangle
   // 64 regs 5.5 vs 48 regs 5.8; 5-clique 48 regs 12.3 vs 64 regs 13.4.
-  constexpr int kMinB = K == 3 ? 8 : K <= 5 ? 10 : 8;
+#ifndef AGPM_FLAT_MINB45
+#define AGPM_FLAT_MINB45 10
+#endif
+  constexpr int kMinB = K == 3 ? 8 : K <= 5 ? AGPM_FLAT_MINB45 : 8;
   auto kern = fr_flat_kernel<K, AGPM_FLAT_U, kMinB, R>;
   static int occ = -1;
   if (occ < 0) {
