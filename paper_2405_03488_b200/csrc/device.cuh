@@ -58,6 +58,8 @@ DeviceCtx& ctx_for_current_device();
 // device-wide synchronisation.
 cudaError_t dev_malloc_bytes(void** p, size_t bytes);
 cudaError_t dev_free(void* p);
+// stream-ordered free of a block only `s` has touched (no device-wide sync)
+cudaError_t dev_free_stream(void* p, cudaStream_t s);
 template <class T>
 cudaError_t dev_malloc(T** p, size_t bytes) {
   return dev_malloc_bytes(reinterpret_cast<void**>(p), bytes);

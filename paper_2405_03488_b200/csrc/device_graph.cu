@@ -86,6 +86,35 @@ cudaError_t dev_free(void* p) {
   }
   return cudaFreeAsync(p, ctx.stream);
 }
+// Free a block only stream `s` has used (temporaries of a view build): stream-
+// ordered, no device-wide synchronisation — a view upload on one host thread
+// then never waits for sampling kernels another thread runs meanwhile.
+cudaError_t dev_free_stream(void* p, cudaStream_t s) {
+  if (!p) return cudaSuccess;
+  size_t bytes = 0;
+  int owner = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_park_mu);
+    auto it = g_big.find(p);
+    if (it != g_big.end()) {
+      bytes = it->second.first;
+      owner = it->second.second;
+      g_big.erase(it);
+    }
+  }
+  if (bytes) {  // a parkable block: park once the stream is done with it
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_park_mu);
+    if (g_parked_bytes + bytes <= kParkCap) {
+      g_parked.push_back({p, bytes, owner});
+      g_parked_bytes += bytes;
+      return cudaSuccess;
+    }
+  }
+  return cudaFreeAsync(p, s);
+}
+
 void count_launch(uint64_t n) { g_launches += n; }
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -266,9 +295,9 @@ void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsig
     AGPM_CUDA(cudaGetLastError());
   }
   AGPM_CUDA(cudaStreamSynchronize(s));
-  AGPM_CUDA(dev_free(deg));
-  AGPM_CUDA(dev_free(prefix));
-  AGPM_CUDA(dev_free(red));
+  AGPM_CUDA(dev_free_stream(deg, s));
+  AGPM_CUDA(dev_free_stream(prefix, s));
+  AGPM_CUDA(dev_free_stream(red, s));
   g->bytes = sizeof(VtxInfo) * (uint64_t)n + 4ull * g->nbr_len + 8ull * arcs;
 }
 
@@ -334,8 +363,9 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
       AGPM_CUDA(cudaMemcpyAsync(g->nbr, neighbors, sizeof(uint32_t) * neighbor_len,
                                 cudaMemcpyHostToDevice, s));
     finalize_view(g, d_begin, d_end, s);
-    AGPM_CUDA(dev_free(d_begin));
-    if (d_end) AGPM_CUDA(dev_free(d_end));
+    AGPM_CUDA(dev_free_stream(d_begin, s));
+    if (d_end) AGPM_CUDA(dev_free_stream(d_end, s));
+    AGPM_CUDA(cudaStreamSynchronize(s));  // the view is complete when the call returns
     *out = g;
   });
 }
