@@ -307,10 +307,8 @@ def run_gpu(args):
     # ---- e2e through the public C-ABI with host buffers (graph upload + fixed budget + read-back)
     # Every step uploads the whole graph from pinned host memory into a fresh
     # device view and runs run_fixed_budget(2^24) on it, reading the moments back.
-    # Two host threads pipeline consecutive steps: the upload of step s+1 (copy
-    # engine, its own stream) overlaps the sampling of step s; the uploader also
-    # frees finished views (a free waits for the device, so it is kept off the
-    # sampling thread).
+    # Two host threads pipeline consecutive steps: the upload of step s+1 runs on
+    # its own thread and stream while step s samples.
     import queue
 
     e2e_steps = max(1, args.steps)  # every timed step, so a single slow host hiccup is amortised like in `value`
@@ -324,40 +322,47 @@ def run_gpu(args):
             return A.run_fixed_budget(dgh, plan, B, seed)
         return A.run_fixed_budget_sharded(comm, dgh, plan, B * world, seed)  # B ids per rank, accumulators gathered
 
-    for _ in range(2):  # untimed warm-up steps at the full budget (allocator / pinned-path first touches)
-        dgh = A.DeviceGraph(g)
-        fixed(dgh, 1)
-        del dgh
+    def pipeline(nsteps, seed0, up_list, run_list):
+        # the uploader thread builds view s+1 while the sampler runs step s and
+        # releases the views the sampler is done with (a free waits for the
+        # device, so it stays off the sampling thread); measured against building
+        # the indexes on the uploader too (prepare(): 1.6e9 samples/s — its kernels
+        # queue behind the resident sampling grid) and against a non-persistent
+        # sampling grid with a high-priority upload stream (1.6e9, sampling slowed)
+        ready, done = queue.Queue(maxsize=1), queue.Queue()
+
+        def uploader():
+            A.lib().agpm_set_device(dev_index)
+            for _ in range(nsteps):
+                while not done.empty():
+                    done.get()
+                t1 = time.perf_counter()
+                v = A.DeviceGraph(g)
+                up_list.append(round((time.perf_counter() - t1) * 1e3, 3))
+                ready.put(v)
+                del v
+
+        th = threading.Thread(target=uploader)
+        th.start()
+        for s in range(nsteps):
+            dgh = ready.get()
+            t2 = time.perf_counter()
+            fixed(dgh, seed0 + s)
+            run_list.append(round((time.perf_counter() - t2) * 1e3, 3))
+            done.put(dgh)
+            del dgh
+        th.join()
+        while not done.empty():
+            done.get()
+
+    # untimed warm-up of the same pipeline (pool / parked-block / pinned-path first touches)
+    pipeline(max(3, args.warmup), 1000, [], [])
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    ready, done = queue.Queue(maxsize=1), queue.Queue()
     up_list, run_list = [], []
-
-    def uploader():
-        A.lib().agpm_set_device(dev_index)
-        for s in range(e2e_steps):
-            while not done.empty():  # release views the sampler finished with
-                done.get()
-            t1 = time.perf_counter()
-            v = A.DeviceGraph(g)
-            up_list.append(round((time.perf_counter() - t1) * 1e3, 3))
-            ready.put(v)
-            del v
-
     t = time.perf_counter()
-    th = threading.Thread(target=uploader)
-    th.start()
-    for s in range(e2e_steps):
-        dgh = ready.get()
-        t2 = time.perf_counter()
-        acc = fixed(dgh, 1 + s)
-        run_list.append(round((time.perf_counter() - t2) * 1e3, 3))
-        done.put(dgh)
-        del dgh
-    th.join()
-    while not done.empty():
-        done.get()
+    pipeline(e2e_steps, 1, up_list, run_list)
     e2e_s = time.perf_counter() - t
     up_s, run_s = sum(up_list) / 1e3, sum(run_list) / 1e3
     if dist is not None:

@@ -152,6 +152,11 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
                       const uint32_t* neighbors, uint64_t neighbor_len, int oriented, void* stream,
                       agpm_graph** out);
 int agpm_graph_upload_host(const agpm_host_graph* g, void* stream, agpm_graph** out);
+/* Build the view's sampling indexes now — the dense-core bit matrix (current
+ * core dimension) and the twin-arc index (4 B per arc, best effort: skipped when
+ * HBM is short) — instead of lazily on its first / second sampling launch.
+ * Samples are identical either way; returns when the indexes are built. */
+int agpm_graph_prepare(agpm_graph* g, void* stream);
 /* page-lock (cudaHostRegister) a host graph's arrays so uploads run at DMA
  * speed; unpinned automatically by agpm_host_graph_free */
 int agpm_host_graph_pin(agpm_host_graph* g);

@@ -113,6 +113,7 @@ def _declare(L):
         "agpm_gen_rmat": (C.c_int, [A.u32, A.u32, C.c_double, C.c_double, C.c_double, A.u64, C.POINTER(A.P)]),
         "agpm_graph_upload": (C.c_int, [A.u32, A.u64, A.pu64, A.pu64, A.pu32, A.u64, C.c_int, A.P, C.POINTER(A.P)]),
         "agpm_graph_upload_host": (C.c_int, [A.P, A.P, C.POINTER(A.P)]),
+        "agpm_graph_prepare": (C.c_int, [A.P, A.P]),
         "agpm_host_graph_pin": (C.c_int, [A.P]),
         "agpm_graph_free": (C.c_int, [A.P]),
         "agpm_graph_info": (C.c_int, [A.P, A.pu32, A.pu64, A.pu64, C.POINTER(C.c_int), A.pu64]),
@@ -406,6 +407,11 @@ class DeviceGraph:
         if h and h.value and _lib is not None:
             _lib.agpm_graph_free(h)
             self._h = None
+
+    def prepare(self, stream=None):
+        """Build the sampling indexes (dense core, twin arcs) now; same samples either way."""
+        _check(lib().agpm_graph_prepare(self._h, stream))
+        return self
 
     def relabel_by_degree(self, stream=None):
         """relabel_by_degree on the device (plain undirected views)."""

@@ -153,6 +153,19 @@ void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
 
 using namespace agpm_b200;
 
+extern "C" int agpm_graph_prepare(agpm_graph* g, void* stream) {
+  // build a view's sampling indexes now (dense-core bit matrix at the configured
+  // dimension, twin arcs) instead of on its first / second sampling launch — e.g.
+  // on an upload thread, overlapped with sampling of another view
+  return guarded([&] {
+    if (!g) throw std::invalid_argument("null argument");
+    DeviceGuard guard(g->device);
+    cudaStream_t s = pick_stream(stream);
+    ensure_core_bits(g, s);
+    ensure_twin_arcs(g, s);
+  });
+}
+
 extern "C" int agpm_ns_set_core_dim(uint32_t dim) {
   return guarded([&] {
     if (dim > 65536) throw std::invalid_argument("core dimension must be <= 65536");

@@ -198,6 +198,11 @@ DeviceCtx& ctx_for_current_device() {
         AGPM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
         uint64_t keep = ~0ull;  // never trim: freed graph memory stays cached for the next view
         AGPM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        // never make an allocation on one stream wait for work pending on another
+        // (a view uploaded on one host thread must not queue behind the sampling
+        // kernels of another); reuse only what is already free
+        int no = 0;
+        AGPM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no));
         g_pool_ready[dev] = true;
       }
     }

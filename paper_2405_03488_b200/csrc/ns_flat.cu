@@ -380,8 +380,17 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
     AGPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kFlatThreads, 0));
     occ = std::max(o, 1);
   }
-  const unsigned blocks = (unsigned)std::max<unsigned long long>(
-      1, std::min<unsigned long long>((L.count + kFlatThreads - 1) / kFlatThreads, (unsigned long long)ctx.sm_count * occ));
+  // AGPM_FLAT_WAVES > 0: at most that many resident waves of blocks (a grid-
+  // stride loop); 0: one block per 128 samples, so blocks retire continuously
+  // and kernels of other streams (a view being uploaded and indexed on another
+  // host thread) are scheduled in between instead of waiting for the launch
+#ifndef AGPM_FLAT_WAVES
+#define AGPM_FLAT_WAVES 1
+#endif
+  const unsigned long long want = (L.count + kFlatThreads - 1) / kFlatThreads;
+  const unsigned long long cap =
+      AGPM_FLAT_WAVES > 0 ? (unsigned long long)ctx.sm_count * occ * AGPM_FLAT_WAVES : want;
+  const unsigned blocks = (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(want, cap));
   kern<<<blocks, kFlatThreads, 0, s>>>(A);
   count_launch();
   AGPM_CUDA(cudaGetLastError());
