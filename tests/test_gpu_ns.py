@@ -270,3 +270,22 @@ def test_twin_arc_hints_same_samples(agpm, oracle, graphs, strat, pattern):
         for v, h, b in runs:
             np.testing.assert_array_equal(v, ov)
             np.testing.assert_array_equal(b, ob)
+
+
+def test_prepare_builds_indexes_same_samples(agpm, oracle, graphs):
+    """agpm_graph_prepare builds the dense core and twin arcs eagerly: the view
+    grows by the twin index at once and draws the oracle's records from its
+    first launch on."""
+    g = graphs["rmat12_rel"]
+    off, nbr = g.arrays()
+    dg = agpm.DeviceGraph(g)
+    before = dg.info()["device_bytes"]
+    dg.prepare()
+    grown = dg.info()["device_bytes"] - before
+    assert grown >= 4 * dg.info()["arcs"]  # twin arcs (+ the dense-core rows)
+    plan = agpm.compile_plan("4clique")
+    v, h, b = agpm.draw_samples(dg, plan, 3, 77, 1 << 18)
+    ov, oh, ob = oracle.draw_records(off, nbr, g.edge_count, plan, 3, 77, 1 << 18)
+    np.testing.assert_array_equal(v, ov)
+    np.testing.assert_array_equal(b, ob)
+    assert dg.info()["device_bytes"] - before == grown  # nothing rebuilt on launch
