@@ -102,6 +102,7 @@ struct agpm_graph {
   uint64_t max_degree = 0;
   bool oriented = false;
   bool plain = true;       // end[u] == begin[u+1] and begin[0] == 0
+  bool loop_free = false;  // no self-loops (checked when the view is built; ingest graphs by construction)
   agpm_b200::VtxInfo* vtx = nullptr;
   uint32_t* nbr = nullptr;
   unsigned long long* seed_arcs = nullptr;

@@ -219,7 +219,8 @@ namespace {
 
 __global__ void vtx_kernel(const unsigned long long* __restrict__ begin,
                            const unsigned long long* __restrict__ end, const uint32_t* __restrict__ nbr,
-                           uint32_t n, VtxInfo* __restrict__ vtx, unsigned long long* __restrict__ deg) {
+                           uint32_t n, VtxInfo* __restrict__ vtx, unsigned long long* __restrict__ deg,
+                           unsigned long long* __restrict__ loops) {
   for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
        u += (uint64_t)gridDim.x * blockDim.x) {
     unsigned long long b = begin[u];
@@ -233,6 +234,7 @@ __global__ void vtx_kernel(const unsigned long long* __restrict__ begin,
       else
         hi = mid;
     }
+    if (lo > b && nbr[lo - 1] == (uint32_t)u) atomicOr(loops, 1ull);  // a self-loop u-u
     VtxInfo v;
     v.begin = b;
     v.deg = (unsigned int)(e - b);
@@ -268,9 +270,12 @@ void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsig
   unsigned long long* prefix = nullptr;
   AGPM_CUDA(dev_malloc(&deg, sizeof(unsigned long long) * ((size_t)n + 1)));
   AGPM_CUDA(dev_malloc(&prefix, sizeof(unsigned long long) * ((size_t)n + 1)));
+  unsigned long long* red = nullptr;
+  AGPM_CUDA(dev_malloc(&red, 2 * sizeof(unsigned long long)));  // [0] max degree, [1] self-loop flag
+  AGPM_CUDA(cudaMemsetAsync(red + 1, 0, sizeof(unsigned long long), s));
   int blocks = ctx.sm_count * 8;
   if (n) {
-    vtx_kernel<<<blocks, 256, 0, s>>>(d_begin, d_end, g->nbr, n, g->vtx, deg);
+    vtx_kernel<<<blocks, 256, 0, s>>>(d_begin, d_end, g->nbr, n, g->vtx, deg, red + 1);
     count_launch();
     AGPM_CUDA(cudaGetLastError());
   }
@@ -279,8 +284,6 @@ void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsig
   size_t tmp_bytes = 0;
   cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, deg, prefix + 1, (int64_t)n, s);
   size_t tmp_bytes2 = 0;
-  unsigned long long* red = nullptr;
-  AGPM_CUDA(dev_malloc(&red, sizeof(unsigned long long)));
   cub::DeviceReduce::Max(nullptr, tmp_bytes2, deg, red, (int64_t)n + 1, s);
   void* tmp = ctx.get(7, std::max(tmp_bytes, tmp_bytes2) + 16);
   if (n) {
@@ -290,9 +293,12 @@ void finalize_view(agpm_graph* g, const unsigned long long* d_begin, const unsig
   AGPM_CUDA(cudaMemcpyAsync(&arcs, prefix + n, sizeof(arcs), cudaMemcpyDeviceToHost, s));
   AGPM_CUDA(cub::DeviceReduce::Max(tmp, tmp_bytes2, deg, red, (int64_t)n + 1, s));
   AGPM_CUDA(cudaMemcpyAsync(&maxd, red, sizeof(maxd), cudaMemcpyDeviceToHost, s));
+  unsigned long long loops = 0;
+  AGPM_CUDA(cudaMemcpyAsync(&loops, red + 1, sizeof(loops), cudaMemcpyDeviceToHost, s));
   AGPM_CUDA(cudaStreamSynchronize(s));
   g->arcs = arcs;
   g->max_degree = maxd;
+  g->loop_free = loops == 0;
   AGPM_CUDA(dev_malloc(&g->seed_arcs, sizeof(unsigned long long) * (size_t)(arcs ? arcs : 1)));
   if (n && arcs) {
     seed_arcs_kernel<<<blocks, 256, 0, s>>>(g->vtx, g->nbr, prefix, n, g->seed_arcs);
@@ -368,6 +374,13 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
       AGPM_CUDA(cudaMemcpyAsync(g->nbr, neighbors, sizeof(uint32_t) * neighbor_len,
                                 cudaMemcpyHostToDevice, s));
     finalize_view(g, d_begin, d_end, s);
+    if (!g->loop_free) {  // the device samplers assume simple graphs (as every builder here produces)
+      AGPM_CUDA(dev_free_stream(d_begin, s));
+      if (d_end) AGPM_CUDA(dev_free_stream(d_end, s));
+      AGPM_CUDA(cudaStreamSynchronize(s));
+      agpm_graph_free(g);
+      throw std::invalid_argument("the graph has self-loops; build it with CsrGraph::from_edges (which drops them)");
+    }
     AGPM_CUDA(dev_free_stream(d_begin, s));
     if (d_end) AGPM_CUDA(dev_free_stream(d_end, s));
     AGPM_CUDA(cudaStreamSynchronize(s));  // the view is complete when the call returns

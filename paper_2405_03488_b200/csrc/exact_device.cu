@@ -284,7 +284,7 @@ unsigned long long run_exact_k(const agpm_graph* gr, const DevPlan& p, bool appl
   DeviceCtx& ctx = ctx_for_current_device();
   // the dense-core bit matrix (core_bits.cu) answers leaves whose lists are core rows
   ensure_core_bits(const_cast<agpm_graph*>(gr), s);
-  GraphArgs g{gr->vtx, gr->nbr, gr->seed_arcs, gr->arcs, gr->plain, nullptr, 0};
+  GraphArgs g{gr->vtx, gr->nbr, gr->seed_arcs, gr->arcs, gr->plain, gr->loop_free, nullptr, 0};
   g.core = gr->core;
   g.core_base = gr->core_base;
   g.core_wpr = gr->core_wpr;

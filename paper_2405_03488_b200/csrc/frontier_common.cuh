@@ -299,7 +299,8 @@ __device__ int advance(const FrontierArgs& A, unsigned long long i, Sample<K, R>
 #pragma unroll
       for (int q = 0; q < K; ++q) {
         ex[q] = INF;
-        if (q < j && S.bnd[q] >= lo && S.bnd[q] < hi) {
+        // the list's own owner is never in it on a loop-free graph: no search
+        if (q < j && S.bnd[q] >= lo && S.bnd[q] < hi && !(A.g.loop_free && q == drv)) {
           const uint32_t o = lb_thread(dptr, 0, dsize, S.bnd[q]);
           if (o < dsize && ldn(dptr, o) == S.bnd[q]) {
             ex[q] = o;

@@ -303,6 +303,7 @@ agpm_graph* view_from_sorted_arcs(DevBuf<unsigned long long>& arcs, uint64_t cou
     g->edge_count = edge_count;
     g->oriented = oriented;
     g->plain = true;
+    g->loop_free = true;  // ingest drops self-loops (their keys sort last and are cut)
     g->nbr_len = count;
     g->arcs = count;
     g->nbr = alloc_nbr(count, s);

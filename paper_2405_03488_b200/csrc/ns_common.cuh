@@ -47,6 +47,7 @@ struct GraphArgs {
   const unsigned long long* __restrict__ seed_arcs;
   unsigned long long arcs;
   int plain;
+  int loop_free;  // no vertex is in its own list (a single-list step's owner never needs a search)
   // dense-core adjacency bit matrix (core_bits.cu): bit (u - core_base, v - core_base)
   // of row-major rows of core_wpr words, for u, v >= core_base; null = off
   const uint32_t* __restrict__ core;

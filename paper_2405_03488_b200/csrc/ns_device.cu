@@ -209,6 +209,7 @@ GraphArgs graph_args(const agpm_graph* g) {
   a.seed_arcs = g->seed_arcs;
   a.arcs = g->arcs;
   a.plain = g->plain;
+  a.loop_free = g->loop_free;
   a.core = g->core;
   a.core_base = g->core_base;
   a.core_wpr = g->core_wpr;

@@ -289,3 +289,19 @@ def test_prepare_builds_indexes_same_samples(agpm, oracle, graphs):
     np.testing.assert_array_equal(v, ov)
     np.testing.assert_array_equal(b, ob)
     assert dg.info()["device_bytes"] - before == grown  # nothing rebuilt on launch
+
+
+def test_self_loops_rejected_at_upload(agpm):
+    """The device path samples simple graphs (every builder — from_edges, the
+    loaders' edge lists, the generators, device ingest — drops self-loops); a CSR
+    handed over with a self-loop is refused loudly at upload, not sampled wrongly."""
+    g = agpm.rmat(10, 8, seed=4).relabel_by_degree()
+    off, nbr = g.arrays()
+    lists = [list(nbr[off[u]:off[u + 1]]) for u in range(len(off) - 1)]
+    lists[5] = sorted(lists[5] + [5])
+    loff = np.zeros(len(lists) + 1, np.uint64)
+    loff[1:] = np.cumsum([len(x) for x in lists])
+    lnbr = np.array([x for li in lists for x in li], np.uint32)
+    with pytest.raises(ValueError, match="self-loops"):
+        agpm.DeviceGraph(begin=loff, neighbors=lnbr, edge_count=g.edge_count)
+    agpm.DeviceGraph(begin=off, neighbors=nbr, edge_count=g.edge_count)  # the same graph without the loop
