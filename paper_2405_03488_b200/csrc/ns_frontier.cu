@@ -264,7 +264,8 @@ __global__ void __launch_bounds__(256) fr_pick_kernel(const FrontierArgs A, int 
 #pragma unroll
       for (int q = 0; q < K; ++q) {
         ex[q] = INF;
-        if (q < j && S.bnd[q] >= lo && S.bnd[q] < hi) {
+        // the driver's own owner is never in it on a loop-free graph
+        if (q < j && S.bnd[q] >= lo && S.bnd[q] < hi && !(A.g.loop_free && (uint32_t)q == dp->drv_pos)) {
           const uint32_t o = lb_thread(D, 0, dsize, S.bnd[q]);
           if (o < dsize && ldn(D, o) == S.bnd[q] && !((words[o >> 5] >> (o & 31)) & 1u)) ex[q] = o;
         }
