@@ -241,7 +241,8 @@ int agpm_ns_set_rng(int policy);
 int agpm_ns_set_frontier_reuse(int on);
 /* frontier only: dimension C of the dense-core adjacency bit matrix (top C ids,
  * C*C/8 bytes, kept in L2) that answers core-core membership tests in one
- * load; 0 disables; default 65536. Results are identical either way. */
+ * load; 0 disables; 0xffffffff = auto (default: 65536 up to 2^21 vertices,
+ * 262144 above when it fits); at most 262144. Results are identical either way. */
 int agpm_ns_set_core_dim(uint32_t dim);
 
 /* Device-pointer building blocks (bench / multi-rank driver): enqueue only.

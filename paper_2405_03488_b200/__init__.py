@@ -659,8 +659,9 @@ def set_strategy(name):
 
 
 def set_core_dim(dim):
-    """Dense-core bit-matrix dimension for the frontier sampler (0 = off, default 65536)."""
-    _check(lib().agpm_ns_set_core_dim(int(dim)))
+    """Dense-core bit-matrix dimension (0 = off; None = auto: 65536 up to 2^21
+    vertices, 262144 above). Samples are identical for every setting."""
+    _check(lib().agpm_ns_set_core_dim(0xFFFFFFFF if dim is None else int(dim)))
 
 
 def set_rng(policy):

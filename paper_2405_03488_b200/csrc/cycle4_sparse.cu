@@ -204,7 +204,7 @@ unsigned long long cycle4_sparse_count(agpm_graph* g, uint32_t tau_id, cudaStrea
   A.tau_id = std::min(tau_id, g->n);
   // pair core: the top P ids, inside the dense-core matrix and above V_s;
   // the triangular table costs 4 P^2 bytes, so P shrinks if HBM is short
-  uint32_t P = g->core ? std::min(g->core_dim, g->n - A.tau_id) : 0u;
+  uint32_t P = g->core ? std::min({65536u, g->core_dim, g->n - A.tau_id}) : 0u;
   size_t free_b = 0, total_b = 0;
   AGPM_CUDA(cudaMemGetInfo(&free_b, &total_b));
   while (P > 1 && 4ull * P * P > free_b / 2) P /= 2;

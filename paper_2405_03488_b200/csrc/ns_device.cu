@@ -240,8 +240,10 @@ bool clique_plan(const DevPlan& p) {
 
 int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count, int forced) {
   if (forced != kStrategyAuto) return forced;
+  // flat up to 2^22 vertices (64 x a 64 K core; measured slower than the frontier
+  // above that, RMAT-24 / -27), whatever the core dimension
   const uint64_t core = core_dim_setting();
-  if (count >= (1ull << 18) && clique_plan(p) && core && g->n <= 64 * core) return kStrategyFlat;
+  if (count >= (1ull << 18) && clique_plan(p) && core && g->n <= (1u << 22)) return kStrategyFlat;
   const double avg_deg = g->n ? static_cast<double>(g->arcs) / g->n : 0.0;
   if (avg_deg <= 24.0 && g->max_degree <= 256) return kStrategyLane;
   return count >= (1ull << 18) ? kStrategyFrontier : kStrategyWarp;

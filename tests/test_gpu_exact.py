@@ -120,5 +120,5 @@ def test_exact_partial_core(agpm, oracle, pattern, core):
     try:
         got = agpm.exact_count(agpm.DeviceGraph(g), plan)
     finally:
-        agpm.set_core_dim(65536)
+        agpm.set_core_dim(None)
     assert got == oracle.exact_count(off, nbr, g.edge_count, plan)

@@ -48,7 +48,7 @@ def strategy(agpm, request):
     yield request.param
     agpm.set_strategy("auto")
     agpm.set_frontier_reuse(False)
-    agpm.set_core_dim(65536)
+    agpm.set_core_dim(None)
 
 
 @pytest.mark.parametrize("name", ["er200", "er200_rel", "er60_dense", "rmat12_rel", "rmat12"])
@@ -88,7 +88,7 @@ def test_long_drivers_bit_exact(agpm, oracle, pattern, relabel, strat):
         v, h, b = agpm.draw_samples(dg, plan, 4, 777, 20000)
     finally:
         agpm.set_strategy("auto")
-        agpm.set_core_dim(65536)
+        agpm.set_core_dim(None)
     ov, oh, ob = oracle.draw_records(off, nbr, g.edge_count, plan, 4, 777, 20000)
     np.testing.assert_array_equal(v, ov)
     np.testing.assert_array_equal(b, ob)

@@ -77,7 +77,7 @@ def test_cycle4_pair_count_equals_wedge_dfs(agpm, core, scale, ef, tau):
         assert res.c_sparse == agpm.exact_count_rooted(dg, plan, res.tau_id)
         assert res.c_sparse + int(res.c_dense) == agpm.exact_count(dg, plan)
     finally:
-        agpm.set_core_dim(65536)
+        agpm.set_core_dim(None)
 
 
 @pytest.mark.slow

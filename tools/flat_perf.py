@@ -20,6 +20,8 @@ patterns = (sys.argv[2] if len(sys.argv) > 2 else "triangle,4clique,5clique").sp
 graphs = (sys.argv[3] if len(sys.argv) > 3 else "rmat20").split(",")
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 B = 1 << 24
+if os.environ.get("AGPM_CORE"):  # dense-core dimension (default 65536)
+    A.set_core_dim(int(os.environ["AGPM_CORE"]))
 st = torch.cuda.Stream()
 torch.cuda.set_stream(st)
 vals = torch.empty(B, dtype=torch.float64, device="cuda")
