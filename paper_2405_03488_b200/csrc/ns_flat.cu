@@ -18,27 +18,79 @@ namespace {
 //   * scalar work (seed, bounds, ranges, driver choice, single-list steps,
 //     picks) runs lane-parallel, exactly as in fr_seed / fr_pick;
 //   * a multi-list step's intersection runs over the CONCATENATION of the
-//     pending samples' driver ranges: element e of the warp's flattened range
-//     goes to lane e % 32, whose segment rank is found from a reduction of
-//     the segment starts (one redux + popc; the fast class reads its driver
-//     and core rows from a rank-indexed shared table), so lanes stay busy
-//     across sample boundaries instead of padding every sample to whole
-//     32-element words; fast samples (every other list a dense-core row, the
-//     driver inside the core) cost one driver load and one bit per list per
-//     element, the rest a generic per-element test;
+//     pending samples' driver ranges, so lanes stay busy across sample
+//     boundaries instead of padding every sample to whole 32-element words.
+//     Fast samples (every other list a dense-core row, the driver inside the
+//     core): the driver ranges are covered by aligned 32-B octets and octet o
+//     of the warp's flattened cover goes to lane o % 32 (fast_round: two 16-B
+//     loads, then one core-row word per element and list; the segment an octet
+//     belongs to comes from a per-group bitmap of segment starts + popc and a
+//     rank-indexed shared table). The rest: element e goes to lane e % 32 and
+//     gets a generic per-element test;
 //   * the live ballots (32 elements per word) land in shared memory; each lane
 //     then counts its own segment, draws r = next_below(|S_j|) from its own
 //     stream (CounterRng, or the optional Philox policy) and selects the r-th
 //     live element — all lanes in parallel.
-// Drivers longer than kFlatW * 32 elements take the warp-cooperative
-// per-sample path of the fused kernel (live_word). Bound vertices inside the
+// Drivers longer than a round (kFlatW * 32 elements) take the warp-cooperative
+// per-sample path (wps_sample). Bound vertices inside the
 // step's [lo, hi) are failed per element (walker.hpp:70-82), so the live count
 // is |S_j| directly.
-constexpr int kFlatW = 64;  // ballot words per warp and round (drivers up to 2048 elements go flat)
+
+constexpr int kFlatW = 64;  // ballot words per warp and round (drivers up to ~2048 elements go flat)
 constexpr int kFlatThreads = 128;
-#ifndef AGPM_FLAT_U
-#define AGPM_FLAT_U 2  // driver words in flight per warp in the fast loop
-#endif
+constexpr int kFlatG = kFlatW / 8;  // groups (256 elements, 8 ballot words) per round
+
+// One round of the fast class. A lane owns one OCTET of the warp's flattened
+// driver range per group: eight consecutive neighbours = one aligned 32-B
+// sector (two 16-B loads), then one core-row word per element and list.
+// gst[g] = {bit b: a segment starts at octet R0 + 32 g + b, rank of the first
+// segment starting in group g or later}; wsrc / wrows by segment rank: the byte
+// address octet 0 of the flattened range would have seen from the segment, and
+// the segment's two core rows. Padding slots (the neighbours of other lists
+// around an unaligned driver range, or the zeroed tail of nbr[]) are probed like
+// any element when they fall inside the core and skipped otherwise; their bits
+// are never counted (the pick phase masks each segment to its own elements).
+template <bool TWO>
+__device__ __forceinline__ void fast_round(const GraphArgs& g, uint32_t R0, uint32_t Rend, int ng, const uint2* gst,
+                                           const unsigned long long* wsrc, const ulonglong2* wrows, uint32_t* bal,
+                                           int lane) {
+  const uint32_t cb = g.core_base, wpr = g.core_wpr;
+  const unsigned le_mask = (2u << lane) - 1u;
+  const uint32_t o0 = R0 + lane;
+#pragma unroll 1
+  for (int i = 0; i < ng; ++i) {
+    uint32_t bits = 0;
+    const uint32_t oct = o0 + 32u * i;
+    if (oct < Rend) {
+      const uint2 st = gst[i];
+      const uint32_t rank = (st.y + __popc(st.x & le_mask) - 1u) & 31u;
+      const uint4* src = reinterpret_cast<const uint4*>(wsrc[rank] + 32ull * oct);
+      const uint4 lo4 = __ldg(src), hi4 = __ldg(src + 1);
+      const ulonglong2 rows = wrows[rank];
+      const uint32_t* row0 = reinterpret_cast<const uint32_t*>(rows.x);
+      const uint32_t* row1 = reinterpret_cast<const uint32_t*>(rows.y);
+      const uint32_t a[8] = {lo4.x - cb, lo4.y - cb, lo4.z - cb, lo4.w - cb,
+                             hi4.x - cb, hi4.y - cb, hi4.z - cb, hi4.w - cb};
+      uint32_t m[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t w = a[k] >> 5;
+        m[k] = 0;
+        if (w < wpr) {
+          m[k] = __ldg(row0 + w);
+          if (TWO) m[k] &= __ldg(row1 + w);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) bits |= ((m[k] >> (a[k] & 31u)) & 1u) << k;
+    }
+    // octet o holds elements 8 o .. 8 o + 7 of the round: word o / 4, byte o % 4
+    uint32_t w = bits << ((lane & 3) * 8);
+    w |= __shfl_xor_sync(FULL, w, 1);
+    w |= __shfl_xor_sync(FULL, w, 2);
+    if ((lane & 3) == 0) bal[8 * i + (lane >> 2)] = w;
+  }
+}
 
 template <int K>
 __device__ __forceinline__ bool flat_live(const GraphArgs& g, const IsectDesc<K>& d, uint32_t a) {
@@ -108,13 +160,14 @@ __device__ __noinline__ WpsOut wps_sample(const GraphArgs g, const IsectDesc<K>*
   return WpsOut{c, rr.ctr, op};
 }
 
-template <int K, int kFlatU, int kMinB, class R = CounterRng>
+template <int K, int kMinB, class R = CounterRng>
 __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const FrontierArgs A) {
   __shared__ IsectDesc<K> sdesc[kFlatThreads];
   __shared__ uint32_t sbal[kFlatThreads / 32][kFlatW];
   __shared__ uint32_t smap[kFlatThreads / 32][32];
-  __shared__ uint4 sfast[kFlatThreads];
-  __shared__ uint32_t sexcl[kFlatThreads];
+  __shared__ unsigned long long ssrc[kFlatThreads];  // by segment rank: byte address of the segment's octet 0 - 32 * segment start
+  __shared__ ulonglong2 srows[kFlatThreads];         // by segment rank: the two core rows
+  __shared__ uint2 sgst[kFlatThreads / 32][kFlatG];  // by round group: {segment-start bits, rank of the first start}
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   IsectDesc<K>* wdesc = sdesc + (threadIdx.x & ~31u);
   IsectDesc<K>& my = wdesc[lane];
@@ -163,7 +216,7 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       __syncwarp();  // descriptors written by advance() are visible to the warp
       const int j = __shfl_sync(FULL, pend, __ffs(pm) - 1) + 2;  // every pending sample is at the same step
       const uint32_t dsz = pend >= 0 ? my.dsize : 0u;
-      const bool wps = dsz > (uint32_t)kFlatW * 32;
+      const bool wps = dsz > (uint32_t)kFlatW * 32 - 16;  // padded to whole octets, a fast driver still fits a round
       unsigned long long cnt = 0;
       uint32_t o_pick = 0;
       // long drivers: the whole warp on one sample, counted, then replayed up to
@@ -191,7 +244,10 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       for (int cls = 0; cls < 2; ++cls) {
       const bool allfast = cls == 0;
       const bool part = pend >= 0 && !wps && fast == allfast;
-      const uint32_t sz = part ? dsz : 0u;
+      // fast class: units are octets of the 32-B-aligned cover of the driver range
+      const uint32_t head = (uint32_t)(reinterpret_cast<unsigned long long>(my.drv) >> 2) & 7u;
+      const uint32_t sz = !part ? 0u : allfast ? (head + dsz + 7) >> 3 : dsz;
+      const uint32_t round_units = allfast ? (uint32_t)kFlatW * 4 : (uint32_t)kFlatW * 32;
       uint32_t P = sz;  // inclusive prefix of segment sizes over lanes
 #pragma unroll
       for (int dd = 1; dd < 32; dd <<= 1) {
@@ -209,54 +265,49 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
         if (allfast) {  // the fast table is indexed by segment rank: no lane lookup in the loop
           const uint32_t l = my.lists;
           const int q0 = __ffs(l) - 1, q1 = 31 - __clz(l);
-          const unsigned long long dp = reinterpret_cast<unsigned long long>(my.drv);
-          sfast[(threadIdx.x & ~31u) + rank] = make_uint4((uint32_t)dp, (uint32_t)(dp >> 32),
-                                                          (my.owner[q0] - cb) * A.g.core_wpr,
-                                                          (my.owner[q1] - cb) * A.g.core_wpr);
-          sexcl[(threadIdx.x & ~31u) + rank] = excl;
+          ssrc[(threadIdx.x & ~31u) + rank] =
+              (reinterpret_cast<unsigned long long>(my.drv) & ~31ull) - 32ull * excl;
+          srows[(threadIdx.x & ~31u) + rank] = make_ulonglong2(
+              reinterpret_cast<unsigned long long>(A.g.core + (unsigned long long)(my.owner[q0] - cb) * A.g.core_wpr),
+              reinterpret_cast<unsigned long long>(A.g.core + (unsigned long long)(my.owner[q1] - cb) * A.g.core_wpr));
         }
       }
       __syncwarp();
       const uint32_t lane_of_rank = smap[wid][lane];
-      const uint4* wfast = sfast + (threadIdx.x & ~31u);
-      const uint32_t* wexcl = sexcl + (threadIdx.x & ~31u);
+      const unsigned long long* wsrc = ssrc + (threadIdx.x & ~31u);
+      const ulonglong2* wrows = srows + (threadIdx.x & ~31u);
+      uint2* gst = sgst[wid];
+      // one or two other lists: the same for every fast sample of the warp (same step, driver among the in-lists)
+      const bool two = __any_sync(FULL, part && allfast && __popc(my.lists) == 2);
       for (uint32_t R0 = 0; R0 < total;) {
-        const uint32_t Rend = __reduce_max_sync(FULL, P <= R0 + (uint32_t)kFlatW * 32 ? P : 0u);
+        const uint32_t Rend = __reduce_max_sync(FULL, P <= R0 + round_units ? P : 0u);
         uint32_t rk = __popc(__ballot_sync(FULL, part && P <= R0));  // segments of earlier rounds
         uint32_t it = 0;
+        const bool inr = part && excl >= R0 && P <= Rend;  // this lane's segment is in the round
+        uint32_t b0 = excl - R0, b1 = P - R0;               // its bits in bal[]
         if (allfast) {
-          // kFlatU independent words in flight per warp: their driver loads, then their bit probes
-          for (uint32_t e0 = R0; e0 < Rend; e0 += 32 * kFlatU, it += kFlatU) {
-            uint32_t a[kFlatU], rw0[kFlatU], rw1[kFlatU];
-            bool v[kFlatU];
+          const int ng = (int)((Rend - R0 + 31) >> 5);
+          if (lane < kFlatG) gst[lane].x = 0;
+          __syncwarp();
+          if (inr) atomicOr(&gst[(excl - R0) >> 5].x, 1u << ((excl - R0) & 31));
+          __syncwarp();
+          {
+            const uint32_t c0 = lane < kFlatG ? __popc(gst[lane].x) : 0u;
+            uint32_t s0 = c0;
 #pragma unroll
-            for (int u = 0; u < kFlatU; ++u) {
-              const uint32_t eb = e0 + 32 * u;
-              const unsigned starts =
-                  __reduce_or_sync(FULL, (part && excl >= eb && excl < eb + 32) ? 1u << (excl - eb) : 0u);
-              const uint32_t rank = rk + __popc(starts & ((2u << lane) - 1u)) - 1u;
-              rk += __popc(starts);
-              const uint4 f = wfast[rank & 31u];
-              const uint32_t ex_src = wexcl[rank & 31u];
-              v[u] = eb + lane < Rend;
-              const uint32_t* drv = reinterpret_cast<const uint32_t*>(((unsigned long long)f.y << 32) | f.x);
-              a[u] = v[u] ? ldo(drv, eb + lane - ex_src) - cb : 0u;
-              rw0[u] = f.z;
-              rw1[u] = f.w;
+            for (int dd = 1; dd < kFlatG; dd <<= 1) {
+              const uint32_t t0 = __shfl_up_sync(FULL, s0, dd);
+              if (lane >= dd) s0 += t0;
             }
-#pragma unroll
-            for (int u = 0; u < kFlatU; ++u) {
-              bool live = false;
-              if (v[u]) {
-                const uint32_t c = a[u];
-                const uint32_t b0 = __ldg(A.g.core + rw0[u] + (c >> 5));
-                const uint32_t b1 = __ldg(A.g.core + rw1[u] + (c >> 5));
-                live = ((b0 & b1) >> (c & 31)) & 1u;
-              }
-              const unsigned b = __ballot_sync(FULL, live);
-              if (lane == 0) bal[it + u] = b;
-            }
+            if (lane < kFlatG) gst[lane].y = rk + s0 - c0;
           }
+          __syncwarp();
+          if (two)
+            fast_round<true>(A.g, R0, Rend, ng, gst, wsrc, wrows, bal, lane);
+          else
+            fast_round<false>(A.g, R0, Rend, ng, gst, wsrc, wrows, bal, lane);
+          b0 = b0 * 8 + head;
+          b1 = b0 + dsz;
         } else
         for (uint32_t e0 = R0; e0 < Rend; e0 += 32, ++it) {
           const unsigned starts =
@@ -275,8 +326,7 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
           if (lane == 0) bal[it] = b;
         }
         __syncwarp();
-        if (part && excl >= R0 && P <= Rend) {  // this lane's segment is in the round
-          const uint32_t b0 = excl - R0, b1 = P - R0;
+        if (inr) {
           const uint32_t w0 = b0 >> 5, w1 = (b1 - 1) >> 5;
           unsigned long long c = 0;
           for (uint32_t w = w0; w <= w1; ++w) c += __popc(bal[w] & seg_mask(w, b0, b1));
@@ -361,16 +411,17 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
     A.step_multi[st] = !(__builtin_popcount(in_m) == 1 && out_m == 0);
     A.step_reuse[st] = 0;
   }
-  // 2 words in flight per warp; registers capped by the resident 128-thread
-  // blocks per SM: the loop is latency bound, so occupancy beats the few spills
-  // a cap costs. Measured per 2^24 samples on the config-2 graph: 4-clique 96
-  // regs 14.2 ms, 64 regs 9.1, 56 regs 8.9, 48 regs 8.8, 40 regs 9.9; triangle
-  // 64 regs 5.5 vs 48 regs 5.8; 5-clique 48 regs 12.3 vs 64 regs 13.4.
+  // Resident 128-thread blocks per SM (the register cap): the kernel hides latency with
+  // warps, but shared memory and local-memory stack compete with L1 for the same 256 KB,
+  // so 8 blocks (64 registers, no spills, 19 KB of tables each) beat 9 and 10.
+  // Measured per 2^24 samples on the config-2 graph (triangle / 4-clique / 5-clique):
+  // 7 blocks 3.35 / 6.05 / 9.99 ms, 8 blocks 3.15 / 5.83 / 9.47, 9 blocks 3.15 / 5.91 / 9.78,
+  // 10 blocks (48 registers, spills) 3.28 / 6.23 / 12.9.
 #ifndef AGPM_FLAT_MINB45
-#define AGPM_FLAT_MINB45 10
+#define AGPM_FLAT_MINB45 8
 #endif
-  constexpr int kMinB = K == 3 ? 8 : K <= 5 ? AGPM_FLAT_MINB45 : 8;
-  auto kern = fr_flat_kernel<K, AGPM_FLAT_U, kMinB, R>;
+  constexpr int kMinB = K <= 5 ? AGPM_FLAT_MINB45 : 8;
+  auto kern = fr_flat_kernel<K, kMinB, R>;
   static int occ = -1;
   if (occ < 0) {
 #ifdef AGPM_FLAT_CARVEOUT
