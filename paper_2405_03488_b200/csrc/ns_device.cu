@@ -225,13 +225,12 @@ constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategy
 std::atomic<int> g_strategy{kStrategyAuto};  // process-wide setting, read once per launch
 
 // clique plans (every step intersects all bound vertices' lists, no out-lists)
-// on graphs whose dense core is a large enough slice (n <= 64 x core dim): their
-// drivers are short suffixes answered by the core, where the flat sampler wins
-// (config-2 graph, per 2^24 samples: triangle 6.2 vs 7.8 ms, 4-clique 8.8 vs
-// 12.5, 5-clique 14.1 vs 18.1; RMAT-22 4-clique 15.1 vs 16.1). Beyond that
-// (RMAT-24: 26.4 vs 22.2 ms, RMAT-27: 79.5 vs 47.2 ms) and for non-clique plans
-// (4-cycle 10.9 vs 9.9 ms, house 170 vs 82) long non-core drivers favour the
-// frontier phases.
+// on graphs up to 2^25 vertices: their drivers are short suffixes answered by
+// the dense core, where the flat sampler wins (per 2^24 4-clique samples, flat vs
+// frontier: RMAT-20 5.8 vs 12.5 ms, RMAT-22 8.6 vs 14.9, RMAT-24 13.1 vs 18.1,
+// RMAT-26 25.5 vs 24.7, RMAT-27 39.8 vs 29.8; 5-clique RMAT-24 17.3 vs 24.8). Beyond
+// that and for non-clique plans (RMAT-22 4-cycle 20.5 vs 10.5 ms: drivers that
+// start below the core) the frontier phases win.
 bool clique_plan(const DevPlan& p) {
   for (int s = 0; s < p.k - 2; ++s)
     if (p.in_mask[s] != (1u << (s + 2)) - 1u || p.out_mask[s] != 0) return false;
@@ -240,10 +239,8 @@ bool clique_plan(const DevPlan& p) {
 
 int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count, int forced) {
   if (forced != kStrategyAuto) return forced;
-  // flat up to 2^22 vertices (64 x a 64 K core; measured slower than the frontier
-  // above that, RMAT-24 / -27), whatever the core dimension
   const uint64_t core = core_dim_setting();
-  if (count >= (1ull << 18) && clique_plan(p) && core && g->n <= (1u << 22)) return kStrategyFlat;
+  if (count >= (1ull << 18) && clique_plan(p) && core && g->n <= (1u << 25)) return kStrategyFlat;
   const double avg_deg = g->n ? static_cast<double>(g->arcs) / g->n : 0.0;
   if (avg_deg <= 24.0 && g->max_degree <= 256) return kStrategyLane;
   return count >= (1ull << 18) ? kStrategyFrontier : kStrategyWarp;
