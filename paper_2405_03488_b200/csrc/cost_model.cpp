@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <future>
 #include <vector>
 
 #include "common.hpp"
@@ -81,9 +82,33 @@ uint64_t count_matches_through_edge_view(const HostView& g, const agpm_plan& p, 
   const int k = p.k;
   uint64_t maps = 0;
   std::vector<uint32_t> image(k, 0);
-  std::vector<uint8_t> used(g.n, 0);
   std::vector<int> ext_order;
   auto nb = [&](uint32_t x) { return g.nbr + g.begin[x]; };
+  // The pool is scanned in ascending order, so membership of its candidates in another
+  // assigned vertex's list is answered by a cursor that only moves forward (gallop, then a
+  // binary search inside the last stride): the same predicate as the reference's
+  // sorted_contains per candidate at a fraction of the cache misses. Injectivity is checked
+  // against the <= k assigned images instead of an n-sized marker array.
+  auto seek = [](const uint32_t* a, uint64_t n, uint64_t& pos, uint32_t x) {
+    if (pos < n && a[pos] < x) {
+      uint64_t lo = pos, step = 1;
+      while (lo + step < n && a[lo + step] < x) {
+        lo += step;
+        step <<= 1;
+      }
+      uint64_t hi = std::min(lo + step, n);
+      ++lo;  // a[lo - 1] < x <= a[hi] (or hi == n)
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] < x)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      pos = lo;
+    }
+    return pos < n && a[pos] == x;
+  };
   std::function<uint64_t(size_t, uint32_t)> extend = [&](size_t depth, uint32_t assigned) -> uint64_t {
     if (depth == ext_order.size()) return 1;
     if (work_budget && *work_budget <= 0) return 0;
@@ -96,21 +121,34 @@ uint64_t count_matches_through_edge_view(const HostView& g, const agpm_plan& p, 
     const uint32_t* pool = nb(image[pool_parent]);
     const uint64_t plen = g.degree(image[pool_parent]);
     if (work_budget) *work_budget -= static_cast<int64_t>(plen);
+    // the other assigned vertices whose lists decide a candidate, with their cursors
+    int chk[AGPM_MAX_K], nchk = 0;
+    bool want[AGPM_MAX_K];
+    uint64_t cur[AGPM_MAX_K];
+    for (int prev = 0; prev < k; ++prev) {
+      if (prev == pool_parent || !((assigned >> prev) & 1u)) continue;
+      const bool w = has_edge(p, prev, pv);
+      if (!w && !p.induced) continue;
+      chk[nchk] = prev;
+      want[nchk] = w;
+      cur[nchk] = 0;
+      ++nchk;
+    }
+    const bool last = depth + 1 == ext_order.size();
     for (uint64_t i = 0; i < plen; ++i) {
       const uint32_t cand = pool[i];
-      if (used[cand]) continue;
       bool ok = true;
-      for (int prev = 0; prev < k && ok; ++prev) {
-        if (prev == pool_parent || !((assigned >> prev) & 1u)) continue;
-        const bool want = has_edge(p, prev, pv);
-        if (!want && !p.induced) continue;
-        if (want != sorted_contains(nb(image[prev]), g.degree(image[prev]), cand)) ok = false;
-      }
+      for (int prev = 0; prev < k && ok; ++prev)
+        if (((assigned >> prev) & 1u) && image[prev] == cand) ok = false;
+      for (int c = 0; c < nchk && ok; ++c)
+        if (want[c] != seek(nb(image[chk[c]]), g.degree(image[chk[c]]), cur[c], cand)) ok = false;
       if (!ok) continue;
+      if (last) {
+        ++total;
+        continue;
+      }
       image[pv] = cand;
-      used[cand] = true;
       total += extend(depth + 1, assigned | (1u << pv));
-      used[cand] = false;
     }
     return total;
   };
@@ -136,9 +174,7 @@ uint64_t count_matches_through_edge_view(const HostView& g, const agpm_plan& p, 
       if (!sorted_contains(nb(da), g.degree(da), db)) continue;
       image[a] = da;
       image[b] = db;
-      used[da] = used[db] = true;
       maps += extend(0, (1u << a) | (1u << b));
-      used[da] = used[db] = false;
     }
   }
   return maps / automorphism_count(p);
@@ -361,21 +397,33 @@ int agpm_count_hybrid(const agpm_host_graph* hg, agpm_graph* g, const agpm_plan*
   return guarded([&] {
     std::memset(out, 0, sizeof(*out));
     const double delta = 1.0 - confidence;
+    uint32_t n = 0;
+    uint64_t m = 0, arcs = 0;
+    agpm_graph_info(g, &n, &m, &arcs, nullptr, nullptr);
+    // gamma probing is host work on the host CSR (budgeted, sequential by definition:
+    // gs_engine.cpp:179-197): it runs on its own thread while the device counts triangles
+    // and profiles; the result is only used when the profile turns out reliable
+    const uint64_t probes = std::min<uint64_t>(1000, std::max<uint64_t>(m, 1));
+    auto gamma_job = std::async(std::launch::async, [&] {
+      return m ? estimate_gamma_host(hg->g, *plan, probes, seed + 17, 50000000) : uint64_t{0};
+    });
+    struct Join {  // the job reads hg / plan: never let it outlive this call
+      std::future<uint64_t>& f;
+      ~Join() {
+        if (f.valid()) f.wait();
+      }
+    } join{gamma_job};
     uint64_t tri = 0;
     if (agpm_triangle_count(g, &tri, stream) != AGPM_OK) throw std::runtime_error(agpm_last_error());
     if (agpm_fast_profile(g, plan, profile_fraction, eps, seed, 1000000, &out->profile, stream) != AGPM_OK)
       throw std::runtime_error(agpm_last_error());
     agpm_keep_probability keep{};
-    uint32_t n = 0;
-    uint64_t m = 0, arcs = 0;
-    agpm_graph_info(g, &n, &m, &arcs, nullptr, nullptr);
     if (!out->profile.reliable) {
       if (agpm_choose_keep_probability(eps, delta, 0.0, 1.0, &keep) != AGPM_OK) throw std::runtime_error(agpm_last_error());
       out->decision = 0;
       out->gamma = 1.0;
     } else {
-      const uint64_t probes = std::min<uint64_t>(1000, std::max<uint64_t>(m, 1));
-      const uint64_t gm = estimate_gamma_host(hg->g, *plan, probes, seed + 17, 50000000);
+      const uint64_t gm = gamma_job.get();
       out->gamma = 2.0 * static_cast<double>(std::max<uint64_t>(1, gm));  // agpm_main.cpp:230-232
       if (agpm_choose_keep_probability(eps, delta, out->profile.scaled_count, out->gamma, &keep) != AGPM_OK)
         throw std::runtime_error(agpm_last_error());
