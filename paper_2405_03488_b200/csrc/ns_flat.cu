@@ -1,5 +1,6 @@
 // Flat sampler (strategy 5): see the comment on fr_flat_kernel.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -160,6 +161,10 @@ __device__ __noinline__ WpsOut wps_sample(const GraphArgs g, const IsectDesc<K>*
   return WpsOut{c, rr.ctr, op};
 }
 
+#ifdef AGPM_FLAT_STATS
+__device__ unsigned long long g_flat_stats[8];
+#endif
+
 template <int K, int kMinB, class R = CounterRng>
 __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const FrontierArgs A) {
   __shared__ IsectDesc<K> sdesc[kFlatThreads];
@@ -238,7 +243,21 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       if (pend >= 0 && !wps) {
         const uint32_t l = my.lists;
         fast = my.core == (l | (1u << 31)) && my.outs == 0 && my.exb == 0 && __popc(l) <= 2;
+#ifdef AGPM_FLAT_STATS
+        const uint32_t exe = my.exb & ~(l | (my.drv_pos < 31 ? 1u << my.drv_pos : 0u));
+        const bool allcore = (my.core & 0x7fffffffu) == l && my.outs == 0 && __popc(l) <= 2;
+        atomicAdd(&g_flat_stats[0], 1ull);
+        atomicAdd(&g_flat_stats[1], (unsigned long long)fast);
+        atomicAdd(&g_flat_stats[2], (unsigned long long)(allcore && (my.core >> 31) && exe == 0));
+        atomicAdd(&g_flat_stats[3], (unsigned long long)(allcore && exe == 0));
+        atomicAdd(&g_flat_stats[4], (unsigned long long)dsz);
+        if (fast) atomicAdd(&g_flat_stats[5], (unsigned long long)dsz);
+        if (allcore && exe == 0) atomicAdd(&g_flat_stats[6], (unsigned long long)dsz);
+#endif
       }
+#ifdef AGPM_FLAT_STATS
+      if (wps) atomicAdd(&g_flat_stats[7], 1ull);
+#endif
       // the rest: flattened element-parallel rounds of <= kFlatW * 32 elements,
       // fast samples first, then the others (each class flattened on its own)
       for (int cls = 0; cls < 2; ++cls) {
@@ -445,6 +464,16 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
   kern<<<blocks, kFlatThreads, 0, s>>>(A);
   count_launch();
   AGPM_CUDA(cudaGetLastError());
+#ifdef AGPM_FLAT_STATS
+  {
+    unsigned long long h[8], z[8] = {};
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(h, g_flat_stats, sizeof(h));
+    cudaMemcpyToSymbol(g_flat_stats, z, sizeof(z));
+    fprintf(stderr, "flat stats: multi-steps %llu fast %llu fast+exb_eff %llu allcore(any lo) %llu | elements %llu fast %llu allcore %llu | wps %llu\n",
+            h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+  }
+#endif
 }
 
 }  // namespace
