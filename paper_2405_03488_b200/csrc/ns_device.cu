@@ -224,23 +224,35 @@ GraphArgs graph_args(const agpm_graph* g) {
 constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategyFrontier = 3, kStrategyFlat = 5;
 std::atomic<int> g_strategy{kStrategyAuto};  // process-wide setting, read once per launch
 
-// clique plans (every step intersects all bound vertices' lists, no out-lists)
-// on graphs up to 2^25 vertices: their drivers are short suffixes answered by
-// the dense core, where the flat sampler wins (per 2^24 4-clique samples, flat vs
-// frontier: RMAT-20 5.8 vs 12.5 ms, RMAT-22 8.6 vs 14.9, RMAT-24 13.1 vs 18.1,
-// RMAT-26 25.5 vs 24.7, RMAT-27 39.8 vs 29.8; 5-clique RMAT-24 17.3 vs 24.8). Beyond
-// that and for non-clique plans (RMAT-22 4-cycle 20.5 vs 10.5 ms: drivers that
-// start below the core) the frontier phases win.
-bool clique_plan(const DevPlan& p) {
-  for (int s = 0; s < p.k - 2; ++s)
-    if (p.in_mask[s] != (1u << (s + 2)) - 1u || p.out_mask[s] != 0) return false;
-  return true;
+// Plans whose multi-list steps all sit in the dense core go to the flat sampler
+// on graphs up to 2^25 vertices: no out-lists and a lower bound above both seed
+// vertices (steps with up to three other lists run in the flat fast class, wider
+// ones per element against the same core rows). Seeds are arc-uniform, hence degree-biased towards the
+// hubs at the top of a relabelled graph, so such drivers are short suffixes
+// inside the core. That covers the clique plans up to the 5-clique's last step
+// and the 4-cycle (S_3 = N(v0) & N(v2) above v1; v2, the owner of one list, may
+// lie inside [lo, hi) but is never in its own list on a loop-free view).
+// Per 2^24 samples, flat vs frontier: 4-clique RMAT-20 5.8 vs 12.5 ms, RMAT-22 8.6 vs
+// 14.9, RMAT-24 13.1 vs 18.1, RMAT-26 25.5 vs 24.7, RMAT-27 39.8 vs 29.8; 5-clique
+// RMAT-24 17.3 vs 24.8; 4-cycle RMAT-20 5.5 vs 8.8, RMAT-22 7.5 vs 11.4, RMAT-24 12.0
+// vs 14.2, RMAT-25 15.9 vs 17.9. Plans without such bounds (house 144 vs 76 ms,
+// dumbbell 35 vs 25, 5-path 8.9 vs 4.0) or with out-lists (4motif-cycle 295 vs 171)
+// and bigger graphs stay on the frontier phases.
+bool core_suffix_plan(const DevPlan& p) {
+  bool multi = false;
+  for (int s = 0; s < p.k - 2; ++s) {
+    const int n_in = __builtin_popcount(p.in_mask[s]);
+    if (n_in == 1 && p.out_mask[s] == 0) continue;  // single-list step: index arithmetic
+    multi = true;
+    if (p.out_mask[s] != 0 || (p.gt_mask[s] & 3u) != 3u) return false;
+  }
+  return multi;
 }
 
 int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count, int forced) {
   if (forced != kStrategyAuto) return forced;
   const uint64_t core = core_dim_setting();
-  if (count >= (1ull << 18) && clique_plan(p) && core && g->n <= (1u << 25)) return kStrategyFlat;
+  if (count >= (1ull << 18) && core_suffix_plan(p) && core && g->n <= (1u << 25)) return kStrategyFlat;
   const double avg_deg = g->n ? static_cast<double>(g->arcs) / g->n : 0.0;
   if (avg_deg <= 24.0 && g->max_degree <= 256) return kStrategyLane;
   return count >= (1ull << 18) ? kStrategyFrontier : kStrategyWarp;

@@ -242,7 +242,12 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       bool fast = false;
       if (pend >= 0 && !wps) {
         const uint32_t l = my.lists;
-        fast = my.core == (l | (1u << 31)) && my.outs == 0 && my.exb == 0 && __popc(l) <= 2;
+        // a bound vertex inside [lo, hi) that owns one of this step's lists cannot be a
+        // candidate on a loop-free view (it is not in its own list): only the others count
+        // (the 4-cycle's S_3 = N(v0) & N(v2) above v1, where v2 itself may exceed v1)
+        const uint32_t own = l | (my.drv_pos < 32 ? 1u << my.drv_pos : 0u);
+        const uint32_t exb = A.g.loop_free ? my.exb & ~own : my.exb;
+        fast = my.core == (l | (1u << 31)) && my.outs == 0 && exb == 0 && __popc(l) <= 2;
 #ifdef AGPM_FLAT_STATS
         const uint32_t exe = my.exb & ~(l | (my.drv_pos < 31 ? 1u << my.drv_pos : 0u));
         const bool allcore = (my.core & 0x7fffffffu) == l && my.outs == 0 && __popc(l) <= 2;
