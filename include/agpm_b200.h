@@ -230,6 +230,9 @@ int agpm_ns_online(agpm_graph* g, const agpm_plan* plan, double eps, double delt
  * picks lane-parallel). All strategies draw identical samples. (4, a fused
  * warp-per-sample-group sampler, was removed: slower than 3 and 5 everywhere.) */
 int agpm_ns_set_strategy(int strategy);
+/* The strategy a sampling launch of `count` ids of `plan` on `g` would run with
+ * the current setting (the auto decision when the setting is 0): one of 1, 2, 3, 5. */
+int agpm_ns_strategy_for(const agpm_graph* g, const agpm_plan* plan, uint64_t count, int* out_strategy);
 /* Per-sample stream policy: 0 = CounterRng(seed, 0, sample_id) (default; the
  * reference's stream, bit-exact with its draw_sample), 1 = Philox4x32-10 keyed by
  * the seed with counter (draw index, sample id) — a counter-based stream of the
@@ -239,10 +242,11 @@ int agpm_ns_set_rng(int policy);
 /* frontier only: let a step whose lists nest the previous step's (cliques)
  * intersect that step's survivors instead of recomputing (same samples). */
 int agpm_ns_set_frontier_reuse(int on);
-/* frontier only: dimension C of the dense-core adjacency bit matrix (top C ids,
- * C*C/8 bytes, kept in L2) that answers core-core membership tests in one
+/* flat and frontier samplers: dimension C of the dense-core adjacency bit matrix
+ * (top C ids, C*C/8 bytes) that answers core-core membership tests in one
  * load; 0 disables; 0xffffffff = auto (default: 65536 up to 2^21 vertices,
- * 262144 above when it fits); at most 262144. Results are identical either way. */
+ * 262144 up to 2^25, 524288 above, when it fits); at most 1048576. Results are
+ * identical either way. */
 int agpm_ns_set_core_dim(uint32_t dim);
 
 /* Device-pointer building blocks (bench / multi-rank driver): enqueue only.

@@ -28,7 +28,7 @@ __all__ = [
     "er_graph", "er_fast", "rmat", "DeviceGraph", "draw_samples", "run_fixed_budget", "run_ns_online",
     "hit_rate_report", "exact_count", "exact_count_rooted", "region_split", "gs_estimate", "choose_keep_probability", "ns_cost_cone",
     "gs_cost_estimate", "select_scheme", "count_matches_through_edge", "estimate_gamma", "fast_profile",
-    "calibrate_hardware_constant", "count_hybrid", "exact_count_shard", "gs_online", "bmin_bytes", "set_strategy", "set_rng", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
+    "calibrate_hardware_constant", "count_hybrid", "exact_count_shard", "gs_online", "bmin_bytes", "set_strategy", "strategy_for", "set_rng", "sample_dev", "window_moments_dev", "kernel_launches", "device_count",
     "Comm", "LocalGroup", "nccl_unique_id", "shard_round", "run_ns_online_sharded", "run_fixed_budget_sharded",
     "exact_count_sharded",
     "Accumulator", "OnlinePolicy", "OnlineResult", "Plan", "Report", "LIB_PATH",
@@ -133,6 +133,7 @@ def _declare(L):
         "agpm_window_moments_dev": (C.c_int, [A.P, A.u64, A.u64, A.P, A.P]),
         "agpm_ns_bmin_bytes": (C.c_int, [A.P, A.pPlan, A.u64, A.u64, A.u64, A.pu64, A.P]),
         "agpm_ns_set_strategy": (C.c_int, [C.c_int]),
+        "agpm_ns_strategy_for": (C.c_int, [A.P, A.pPlan, A.u64, C.POINTER(C.c_int)]),
         "agpm_exact_count": (C.c_int, [A.P, A.pPlan, A.pu64, A.P]),
         "agpm_exact_count_shard": (C.c_int, [A.P, A.pPlan, A.u32, A.u32, A.pu64, A.P]),
         "agpm_gs_online": (C.c_int, [A.P, A.pPlan, A.u32, C.c_double, C.c_double, A.u64, A.u64,
@@ -653,6 +654,13 @@ def window_moments_dev(d_values_ptr, count, window, d_out_ptr, stream=None):
 STRATEGIES = {"auto": 0, "warp": 1, "lane": 2, "frontier": 3, "flat": 5}
 
 
+def strategy_for(dg, plan, count):
+    """Name of the sampler a launch of `count` ids would run under the current setting."""
+    out = C.c_int(0)
+    _check(lib().agpm_ns_strategy_for(dg._h, C.byref(plan), count, C.byref(out)))
+    return {v: k for k, v in STRATEGIES.items()}[out.value]
+
+
 def set_strategy(name):
     """Sampler kernel choice (all draw identical samples): auto | warp | lane | frontier | flat."""
     _check(lib().agpm_ns_set_strategy(STRATEGIES[name]))
@@ -660,7 +668,7 @@ def set_strategy(name):
 
 def set_core_dim(dim):
     """Dense-core bit-matrix dimension (0 = off; None = auto: 65536 up to 2^21
-    vertices, 262144 above). Samples are identical for every setting."""
+    vertices, 262144 up to 2^25, 524288 above). Samples are identical for every setting."""
     _check(lib().agpm_ns_set_core_dim(0xFFFFFFFF if dim is None else int(dim)))
 
 

@@ -118,28 +118,46 @@ void ensure_twin_arcs(agpm_graph* g, cudaStream_t s) {
 void set_core_dim(uint32_t dim) { g_core_dim = dim; }
 uint32_t core_dim_setting() { return g_core_dim; }
 
-// Core dimension for a view. Auto: 65 536 up to 2^21 vertices; 262 144 above,
-// where hub rows outside a 64 K core are common — measured per 2^24 samples,
-// 64 K -> 256 K core: RMAT-27 4-clique 41.8 -> 29.8 ms, 4-cycle 39.2 -> 29.1,
-// RMAT-22 4-clique (flat) 13.2 -> 12.0, 4-cycle 11.2 -> 10.3, while RMAT-20 gains
-// < 1 % for a matrix 16x larger (rebuilt with every fresh view). The larger
-// matrix (8 GB) is only taken when it leaves most of the device free.
+// Core dimension for a view. Auto: 65 536 up to 2^21 vertices; 262 144 up to 2^25
+// and 524 288 above, where hub rows outside a smaller core are common — measured per
+// 2^24 samples, 64 K -> 256 K core: RMAT-27 4-clique 41.8 -> 29.8 ms, 4-cycle 39.2 ->
+// 29.1, RMAT-22 4-clique (flat) 13.2 -> 12.0, 4-cycle 11.2 -> 10.3, while RMAT-20 gains
+// < 1 % for a matrix 16x larger (rebuilt with every fresh view); 256 K -> 512 K core:
+// RMAT-27 4-clique frontier 29.7 -> 28.0 ms, flat 39.8 -> 31.6; RMAT-26 flat 25.4 -> 22.3
+// (frontier 24.0 -> 24.3). The larger matrices (8 GB / 32 GB) are only taken when
+// they leave most of the device free.
 uint32_t core_dim_for(const agpm_graph* g) {
   const uint32_t set = g_core_dim.load();
   if (set != kCoreAuto) return std::min(set, g->n);
-  uint32_t dim = g->n > (1u << 21) ? 262144u : 65536u;
+  uint32_t dim = g->n > (1u << 25) ? 524288u : g->n > (1u << 21) ? 262144u : 65536u;
   if (dim > 65536u) {
+    // blocks the stream-ordered pool still caches (ingest temporaries) count as free
     size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || (size_t)dim * dim / 8 > free_b / 4) {
-      cudaGetLastError();
-      dim = 65536u;
+    cudaMemPool_t pool;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      size_t reserved = 0, used = 0;
+      if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+        free_b = reserved - used;
     }
+    size_t dev_free_b = 0;
+    if (cudaMemGetInfo(&dev_free_b, &total_b) == cudaSuccess) {
+      free_b += dev_free_b;
+    } else {
+      cudaGetLastError();
+      free_b = 0;
+    }
+    while (dim > 65536u && (size_t)dim * dim / 8 > free_b / 3) dim /= 2;
+    if (dim < 262144u) dim = 65536u;
   }
   return std::min(dim, g->n);
 }
 
 // Published after its build finished, under the view's index lock (see ensure_twin_arcs).
 void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
+  const bool autodim = g_core_dim.load() == kCoreAuto;
+  if (g->core && autodim && g->core_auto) return;  // the auto choice is made once per view
   const uint32_t want = g->oriented || !g->plain ? 0u : core_dim_for(g);
   if (g->core && g->core_dim == want) return;
   std::lock_guard<std::mutex> lk(g->index_mu);
@@ -169,6 +187,7 @@ void ensure_core_bits(agpm_graph* g, cudaStream_t s) {
   g->core_base = base;
   g->core_wpr = wpr;
   g->core_dim = want;
+  g->core_auto = autodim;
   g->bytes += 4ull * wpr * want;
 }
 
@@ -191,9 +210,9 @@ extern "C" int agpm_graph_prepare(agpm_graph* g, void* stream) {
 
 extern "C" int agpm_ns_set_core_dim(uint32_t dim) {
   return guarded([&] {
-    // row offsets of the flat sampler's fast table are 32-bit: dim * dim / 32 < 2^32
-    // (0xffffffff = auto, see core_dim_for)
-    if (dim > 262144 && dim != kCoreAuto) throw std::invalid_argument("core dimension must be <= 262144");
+    // 0xffffffff = auto, see core_dim_for; the build kernel keeps one row (dim / 8 bytes)
+    // in shared memory
+    if (dim > 1048576 && dim != kCoreAuto) throw std::invalid_argument("core dimension must be <= 1048576");
     set_core_dim(dim);
   });
 }

@@ -225,7 +225,7 @@ constexpr int kStrategyAuto = 0, kStrategyWarp = 1, kStrategyLane = 2, kStrategy
 std::atomic<int> g_strategy{kStrategyAuto};  // process-wide setting, read once per launch
 
 // Plans whose multi-list steps all sit in the dense core go to the flat sampler
-// on graphs up to 2^25 vertices: no out-lists and a lower bound above both seed
+// on graphs up to 2^26 vertices: no out-lists and a lower bound above both seed
 // vertices (steps with up to three other lists run in the flat fast class, wider
 // ones per element against the same core rows). Seeds are arc-uniform, hence degree-biased towards the
 // hubs at the top of a relabelled graph, so such drivers are short suffixes
@@ -233,7 +233,7 @@ std::atomic<int> g_strategy{kStrategyAuto};  // process-wide setting, read once 
 // and the 4-cycle (S_3 = N(v0) & N(v2) above v1; v2, the owner of one list, may
 // lie inside [lo, hi) but is never in its own list on a loop-free view).
 // Per 2^24 samples, flat vs frontier: 4-clique RMAT-20 5.8 vs 12.5 ms, RMAT-22 8.6 vs
-// 14.9, RMAT-24 13.1 vs 18.1, RMAT-26 25.5 vs 24.7, RMAT-27 39.8 vs 29.8; 5-clique
+// 14.9, RMAT-24 13.1 vs 18.1, RMAT-26 (512 K core) 22.3 vs 24.3, RMAT-27 31.6 vs 28.0; 5-clique
 // RMAT-24 17.3 vs 24.8; 4-cycle RMAT-20 5.5 vs 8.8, RMAT-22 7.5 vs 11.4, RMAT-24 12.0
 // vs 14.2, RMAT-25 15.9 vs 17.9. Plans without such bounds (house 144 vs 76 ms,
 // dumbbell 35 vs 25, 5-path 8.9 vs 4.0) or with out-lists (4motif-cycle 295 vs 171)
@@ -252,7 +252,7 @@ bool core_suffix_plan(const DevPlan& p) {
 int choose_strategy(const agpm_graph* g, const DevPlan& p, uint64_t count, int forced) {
   if (forced != kStrategyAuto) return forced;
   const uint64_t core = core_dim_setting();
-  if (count >= (1ull << 18) && core_suffix_plan(p) && core && g->n <= (1u << 25)) return kStrategyFlat;
+  if (count >= (1ull << 18) && core_suffix_plan(p) && core && g->n <= (1u << 26)) return kStrategyFlat;
   const double avg_deg = g->n ? static_cast<double>(g->arcs) / g->n : 0.0;
   if (avg_deg <= 24.0 && g->max_degree <= 256) return kStrategyLane;
   return count >= (1ull << 18) ? kStrategyFrontier : kStrategyWarp;
@@ -451,6 +451,14 @@ int agpm_ns_set_rng(int policy) {
   return guarded([&] {
     if (policy != 0 && policy != 1) throw std::invalid_argument("rng policy must be 0 (CounterRng) or 1 (Philox4x32-10)");
     g_rng_policy = policy;
+  });
+}
+
+int agpm_ns_strategy_for(const agpm_graph* g, const agpm_plan* plan, uint64_t count, int* out_strategy) {
+  return guarded([&] {
+    if (!g || !plan || !out_strategy) throw std::invalid_argument("null argument");
+    const DevPlan dp = make_dev_plan(g, plan);
+    *out_strategy = choose_strategy(g, dp, count, g_strategy.load(std::memory_order_relaxed));
   });
 }
 

@@ -8,6 +8,9 @@
 #define AGPM_FLAT_DESC_ALIGN 16
 #endif
 #define AGPM_DESC_ALIGN AGPM_FLAT_DESC_ALIGN
+#ifndef AGPM_FLAT_HINT_LOCAL_K
+#define AGPM_FLAT_HINT_LOCAL_K 4
+#endif
 #include "frontier_common.cuh"
 
 namespace agpm_b200 {
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
             // stack) instead of competing for the 48 registers of the hot loop —
             // measured per 2^24 samples: 4-clique 8.15 -> 7.75 ms, 5-clique 11.8 ->
             // 10.6 ms; K = 3 keeps them in registers (triangle 5.13 vs 5.38 ms).
-            if constexpr (K >= 4) {
+            if constexpr (K >= AGPM_FLAT_HINT_LOCAL_K) {
               S.hbo[j] = tw;
               S.hbl[j] = from + 1;
             } else {

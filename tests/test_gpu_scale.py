@@ -1,13 +1,14 @@
 """GPU parity at the big configs' own scale (BASELINE.json configs 3 and 5).
 
-The samplers that only run on big graphs — the frontier phases (non-clique
-plans; clique plans above 2^25 vertices), hub-list
+The samplers that only run on big graphs — the frontier phases (plans that are not
+core suffixes; any plan above 2^26 vertices), hub-list
 (long-driver) paths, the partial dense core, the twin-arc hints (built on a
 view's second sampling launch) — are pinned here against the oracle on the
 graphs themselves, not on scaled-down stand-ins:
 
-* config 3: RMAT-22 ef16 relabelled, 4-cycle (+ 4-clique on the flat and
-  frontier samplers);
+* config 3: RMAT-22 ef16 relabelled, 4-cycle on the flat (auto: the fast class
+  with bound list owners inside [lo, hi)), frontier and warp samplers, 4-clique on
+  flat and frontier, the house (auto = frontier);
 * config 5 class: RMAT-25 ef16 relabelled, 4-clique on the flat (auto) and the
   frontier samplers, and RMAT-27 itself (auto = frontier) when the host can hold
   the oracle's copy of the 4.2 B-arc CSR.
@@ -66,13 +67,16 @@ def rmat22(agpm):
     return _graph(agpm, 22)
 
 
-@pytest.mark.parametrize("spec,strategy", [("4cycle", "auto"), ("4clique", "auto"), ("4clique", "frontier"),
-                                           ("4cycle", "warp"), ("triangle", "auto")])
+@pytest.mark.parametrize("spec,strategy", [("4cycle", "auto"), ("4cycle", "frontier"), ("4clique", "auto"),
+                                           ("4clique", "frontier"), ("4cycle", "warp"), ("triangle", "auto"),
+                                           ("house", "auto")])
 def test_config3_records(agpm, oracle, rmat22, spec, strategy):
     dg, host, info = rmat22
     plan = agpm.compile_plan(spec)
     agpm.set_strategy(strategy)
     try:
+        if strategy == "auto":  # core-suffix plans (cliques, the 4-cycle) run flat, the rest on the frontier phases
+            assert agpm.strategy_for(dg, plan, COUNT) == ("frontier" if spec == "house" else "flat")
         hits = [_records_equal(agpm, oracle, dg, host, info["edge_count"], plan, f, COUNT) for f in OFFSETS]
     finally:
         agpm.set_strategy("auto")
@@ -93,7 +97,7 @@ def rmat25(agpm):
 @pytest.mark.parametrize("spec,strategy", [("4clique", "auto"), ("4clique", "frontier"), ("4cycle", "auto")])
 def test_config5_class_records(agpm, oracle, rmat25, spec, strategy):
     dg, host, info = rmat25
-    assert info["vertex_count"] == 1 << 25  # the largest graph whose clique plans the auto strategy sends to flat
+    assert info["vertex_count"] == 1 << 25  # 256 K core; the auto strategy sends core-suffix plans to flat up to 2^26
     plan = agpm.compile_plan(spec)
     agpm.set_strategy(strategy)
     try:

@@ -27,7 +27,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--repeats", type=int, default=3)
     ap.add_argument("--strategy", default="auto")
-    ap.add_argument("--core", type=int, default=65536)
+    ap.add_argument("--core", type=int, default=-1, help="dense-core dimension; -1 = auto")
     ap.add_argument("--skip-online", action="store_true")
     args = ap.parse_args()
     import torch
@@ -40,7 +40,7 @@ def main():
     info = dg.info()
     plan = agpm.compile_plan(args.pattern)
     agpm.set_strategy(args.strategy)
-    agpm.set_core_dim(args.core)
+    agpm.set_core_dim(None if args.core < 0 else args.core)
     runs = []
     for r in range(0 if args.skip_online else args.repeats):
         agpm.sync()
@@ -72,7 +72,8 @@ def main():
     except Exception:
         pass
     print(json.dumps({"workload": f"rmat{args.scale}_ef{args.edge_factor}_relabelled_{args.pattern}",
-                      "strategy": args.strategy, "core_dim": args.core,
+                      "strategy": args.strategy, "strategy_run": agpm.strategy_for(dg, plan, B),
+                      "core_dim": "auto" if args.core < 0 else args.core,
                       "ingest_seconds": t_ingest, "graph": info,
                       "free_gb_after_ingest": torch.cuda.mem_get_info()[0] / 1e9, "online": runs,
                       "fixed_budget": {"samples": B, "ms": ms, "samples_per_s": B / (ms / 1e3),
