@@ -8,7 +8,7 @@ strategy = sys.argv[1] if len(sys.argv) > 1 else "frontier"
 pattern = sys.argv[2] if len(sys.argv) > 2 else "4clique"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 core = int(sys.argv[4]) if len(sys.argv) > 4 else 16384
-A.set_core_dim(core)
+A.set_core_dim(None if core < 0 else core)  # -1 = auto
 graph = sys.argv[5] if len(sys.argv) > 5 else "rmat20"
 if graph == "er10k":  # config 1
     g = A.er_graph(10000, 20 / 9999, 1).relabel_by_degree()
