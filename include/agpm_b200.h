@@ -154,7 +154,8 @@ int agpm_graph_upload(uint32_t n, uint64_t edge_count, const uint64_t* begin, co
 int agpm_graph_upload_host(const agpm_host_graph* g, void* stream, agpm_graph** out);
 /* Build the view's sampling indexes now — the dense-core bit matrix (current
  * core dimension) and the twin-arc index (4 B per arc, best effort: skipped when
- * HBM is short) — instead of lazily on its first / second sampling launch.
+ * HBM is short) — instead of lazily: the core on the view's first flat / frontier
+ * launch, the twin index once as many ids as the view has arcs have been sampled on it.
  * Samples are identical either way; returns when the indexes are built. */
 int agpm_graph_prepare(agpm_graph* g, void* stream);
 /* page-lock (cudaHostRegister) a host graph's arrays so uploads run at DMA

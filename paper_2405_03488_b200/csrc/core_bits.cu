@@ -197,7 +197,7 @@ using namespace agpm_b200;
 
 extern "C" int agpm_graph_prepare(agpm_graph* g, void* stream) {
   // build a view's sampling indexes now (dense-core bit matrix at the configured
-  // dimension, twin arcs) instead of on its first / second sampling launch — e.g.
+  // dimension, twin arcs) instead of lazily (first launch / after `arcs` sampled ids) — e.g.
   // on an upload thread, overlapped with sampling of another view
   return guarded([&] {
     if (!g) throw std::invalid_argument("null argument");

@@ -110,7 +110,7 @@ struct agpm_graph {
   uint32_t core_base = 0, core_wpr = 0, core_dim = 0;
   bool core_auto = false;  // core_dim was the auto choice (kept: the choice depends on free memory at build time)
   uint32_t* twin = nullptr;  // twin[i] = position of u in N(v) for arc i = (u -> v); plain views, on demand
-  std::atomic<uint32_t> sample_calls{0};  // sampling launches on this view (the twin index is built on reuse)
+  std::atomic<uint64_t> samples_drawn{0};  // ids sampled on this view by the flat / frontier samplers (twin index trigger)
   std::mutex index_mu;  // serialises the lazy index builds (core bits, twin arcs) of this view
   uint64_t bytes = 0;
 };

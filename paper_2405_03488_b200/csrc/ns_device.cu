@@ -287,11 +287,16 @@ void enqueue_sample(const agpm_graph* g, const DevPlan& dp, uint64_t seed, uint6
   }
   const int strat = d_bytes ? kStrategyWarp : choose_strategy(g, dp, count, forced);  // B_min replay: warp kernel
   if (strat == kStrategyFrontier || strat == kStrategyFlat) ensure_core_bits(const_cast<agpm_graph*>(g), s);
-  // the twin-arc index (4 B per arc; 0.4 ms to build on RMAT-20) hints both seed
-  // lists; it pays when a view is sampled more than once, so it is built on the
-  // view's second sampling launch (same samples with or without it)
-  if ((strat == kStrategyFrontier || strat == kStrategyFlat) && ++const_cast<agpm_graph*>(g)->sample_calls >= 2)
-    ensure_twin_arcs(const_cast<agpm_graph*>(g), s);
+  // The twin-arc index (4 B per arc, one binary search per arc to build: 1.0 ms on
+  // RMAT-20, 0.94 s on RMAT-27) hints both seed lists and saves 25-120 ps per sample,
+  // so it pays for itself after about as many samples as the view has arcs: it is
+  // built once that many ids have been sampled on the view (same samples with or
+  // without it; agpm_graph_prepare builds it at once). A one-shot online run on a
+  // big graph (config 5: 1.3 M samples, 4.2 G arcs) never pays the build.
+  if (strat == kStrategyFrontier || strat == kStrategyFlat) {
+    auto* gm = const_cast<agpm_graph*>(g);
+    if (gm->samples_drawn.fetch_add(count, std::memory_order_relaxed) >= g->arcs) ensure_twin_arcs(gm, s);
+  }
   SampleLaunch L{graph_args(g), dp, seed, first, count, d_values, d_bindings, cursor, d_bytes};
   if (strat == kStrategyLane)
     launch_ns_lane(L, s);

@@ -2,8 +2,8 @@
 
 The samplers that only run on big graphs — the frontier phases (plans that are not
 core suffixes; any plan above 2^26 vertices), hub-list
-(long-driver) paths, the partial dense core, the twin-arc hints (built on a
-view's second sampling launch) — are pinned here against the oracle on the
+(long-driver) paths, the partial dense core, the twin-arc hints (built by
+prepare() here; lazily only after `arcs` sampled ids) — are pinned here against the oracle on the
 graphs themselves, not on scaled-down stand-ins:
 
 * config 3: RMAT-22 ef16 relabelled, 4-cycle on the flat (auto: the fast class
@@ -83,6 +83,23 @@ def test_config3_records(agpm, oracle, rmat22, spec, strategy):
     assert sum(hits) > 0
 
 
+@pytest.mark.parametrize("spec,strategy", [("4cycle", "auto"), ("4cycle", "frontier"), ("4clique", "auto"),
+                                           ("4clique", "frontier")])
+def test_config3_records_with_twin_hints(agpm, oracle, rmat22, spec, strategy):
+    """The same records once the view's twin-arc index exists (built lazily only
+    after `arcs` sampled ids; prepare() builds it now): hinted seed ranges at scale."""
+    dg, host, info = rmat22
+    before = dg.info()["device_bytes"]
+    dg.prepare()
+    assert dg.info()["device_bytes"] >= before  # grows by 4 B per arc on the first call
+    plan = agpm.compile_plan(spec)
+    agpm.set_strategy(strategy)
+    try:
+        _records_equal(agpm, oracle, dg, host, info["edge_count"], plan, OFFSETS[1], COUNT)
+    finally:
+        agpm.set_strategy("auto")
+
+
 def test_config3_online(agpm, oracle, rmat22):
     dg, host, info = rmat22
     r = _online_equal(agpm, oracle, dg, host, info["edge_count"], agpm.compile_plan("4cycle"))
@@ -109,6 +126,8 @@ def test_config5_class_records(agpm, oracle, rmat25, spec, strategy):
 
 def test_config5_class_online(agpm, oracle, rmat25):
     dg, host, info = rmat25
+    dg.prepare()  # twin-arc hints on: the online run and the records after it use them
+    _records_equal(agpm, oracle, dg, host, info["edge_count"], agpm.compile_plan("4clique"), OFFSETS[2], COUNT)
     _online_equal(agpm, oracle, dg, host, info["edge_count"], agpm.compile_plan("4clique"))
 
 

@@ -49,7 +49,9 @@ def main():
         agpm.sync()
         runs.append({"seconds": time.perf_counter() - t0, "n": res.report.n, "estimate": res.report.mu,
                      "rel_err_bound": res.report.epsilon_hat, "converged": bool(res.report.converged)})
-    # fixed-budget throughput: 2^24-sample launches, CUDA events on the launching stream
+    # fixed-budget throughput: 2^24-sample launches, CUDA events on the launching stream;
+    # steady state (twin-arc index built: it is otherwise built after `arcs` sampled ids)
+    dg.prepare()
     B = 1 << 24
     vals = torch.empty(B, dtype=torch.float64, device="cuda")
     st = torch.cuda.Stream()

@@ -30,6 +30,7 @@ for graph in graphs:
         dg = A.DeviceGraph(A.er_graph(10000, 20 / 9999, 1).relabel_by_degree(), stream=st.cuda_stream)
     else:
         dg = A.rmat_device(int(graph[4:]), 16, seed=1, stream=st.cuda_stream)
+    dg.prepare()  # dense core + twin-arc index (steady state)
     for strategy in strategies:
         A.set_strategy(strategy)
         for pattern in patterns:

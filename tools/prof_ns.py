@@ -16,6 +16,8 @@ if graph == "er10k":  # config 1
 else:  # built on the device (== the host builder, tests/test_gpu_ingest.py)
     dg = A.rmat_device(int(graph[4:]), 16, seed=1)
 plan = A.compile_plan(pattern)
+if not os.environ.get("AGPM_NO_PREPARE"):
+    dg.prepare()  # steady state: dense core + twin-arc index built before the timed launches
 A.set_strategy(strategy)
 if os.environ.get("AGPM_RNG"):
     A.set_rng(os.environ["AGPM_RNG"])
