@@ -41,8 +41,8 @@ struct DeviceCtx {
   int sm_count = 0;
   cudaStream_t stream = nullptr;
   // grow-only scratch
-  void* scratch[12] = {nullptr};
-  size_t scratch_bytes[12] = {0};
+  void* scratch[16] = {nullptr};
+  size_t scratch_bytes[16] = {0};
   void* pinned[4] = {nullptr};
   size_t pinned_bytes[4] = {0};
   void* get(int slot, size_t bytes);

@@ -64,6 +64,8 @@ struct FrontierArgs {
   // outputs
   double* values;
   uint32_t* bindings;
+  // flat sampler: processing order of the launch's ids (nullptr = id order), see ns_flat.cu
+  const uint32_t* order;
 };
 
 __device__ __forceinline__ uint32_t lb_thread(const uint32_t* base, uint32_t lo, uint32_t hi, uint32_t x) {

@@ -55,6 +55,7 @@ struct GraphArgs {
   uint32_t core_wpr;
   // twin arcs (core_bits.cu): position of u in N(v) for arc (u -> v); null = off
   const uint32_t* __restrict__ twin;
+  uint32_t n;  // vertices
 };
 
 // u, v >= core_base required

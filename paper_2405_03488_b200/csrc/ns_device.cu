@@ -214,6 +214,7 @@ GraphArgs graph_args(const agpm_graph* g) {
   a.core_base = g->core_base;
   a.core_wpr = g->core_wpr;
   a.twin = g->twin;
+  a.n = g->n;
   return a;
 }
 

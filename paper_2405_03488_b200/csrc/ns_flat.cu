@@ -1,4 +1,6 @@
 // Flat sampler (strategy 5): see the comment on fr_flat_kernel.
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -184,8 +186,9 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   for (unsigned long long base = (blockIdx.x * (unsigned long long)blockDim.x) + (threadIdx.x & ~31u);
        base < A.count; base += stride) {
-    const unsigned long long i = base + lane;
-    const bool act = i < A.count;
+    const unsigned long long pos = base + lane;
+    const bool act = pos < A.count;
+    const unsigned long long i = act && A.order ? __ldg(A.order + pos) : pos;
     Sample<K, R> S(A.seed, A.first_id + (act ? i : 0));
     int pend = -1;
     if (act) {
@@ -422,6 +425,63 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
   }
 }
 
+// Processing order. Sample ids are independent streams, so the order in which a
+// launch works through them is free. Sorted by a seed vertex, consecutive samples
+// (the 32 lanes of a warp, the warps of a block) share that hub: its vertex
+// record, its adjacency list and its dense-core row are then read through L1 / L2
+// instead of DRAM. One pre-pass draws every id's seed arc (the same draw the
+// sampler repeats), a partial radix sort on the key's top bits orders the ids
+// (≈ 0.3 ms per 2^24 ids). Taken where it pays: plans with at least two
+// multi-list steps on graphs whose 64 K dense core stays L2-resident (n <= 2^21)
+// — per 2^24 samples on RMAT-20, id order vs sorted by the smaller seed endpoint:
+// 4-clique 5.91 -> 5.72 ms, 5-clique 9.64 -> 8.26; not the triangle (3.16 -> 3.45)
+// or the 4-cycle (5.01 -> 5.05), nor RMAT-22 / 24 with their 8 GB cores (4-clique
+// 8.55 -> 8.86, 4-cycle 7.06 -> 7.74). Sorting by the larger endpoint: 5.70 / 8.84;
+// 12 or 8 key bits instead of 16: 5.99 / 8.61, 5.87 / 8.56. Values and bindings are
+// written by id, so results do not depend on the order.
+#ifndef AGPM_FLAT_SORT_KEY
+#define AGPM_FLAT_SORT_KEY 0  // -1 off, 0 smaller seed endpoint, 1 larger seed endpoint
+#endif
+#ifndef AGPM_FLAT_SORT_BITS
+#define AGPM_FLAT_SORT_BITS 16
+#endif
+template <class R>
+__global__ void flat_seedkey_kernel(GraphArgs g, unsigned long long seed, unsigned long long first_id,
+                                    unsigned long long count, uint32_t* __restrict__ keys,
+                                    uint32_t* __restrict__ idx) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < count;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    R rng(seed, 0, first_id + i);
+    const unsigned long long arc = __ldg(g.seed_arcs + rng.next_below(g.arcs));
+    const uint32_t u = (uint32_t)(arc >> 32), v = (uint32_t)arc;
+    keys[i] = AGPM_FLAT_SORT_KEY == 0 ? min(u, v) : max(u, v);
+    idx[i] = (uint32_t)i;
+  }
+}
+
+template <class R>
+const uint32_t* flat_order(const SampleLaunch& L, uint32_t n_vertices, int multi_steps, cudaStream_t s) {
+  if (AGPM_FLAT_SORT_KEY < 0 || multi_steps < 2 || n_vertices > (1u << 21) || L.count < (1ull << 20) ||
+      L.count > 0xffffffffull)
+    return nullptr;
+  DeviceCtx& ctx = ctx_for_current_device();
+  const size_t n = (size_t)L.count;
+  auto* buf = static_cast<uint32_t*>(ctx.get(12, 16 * n));  // keys in/out, idx in/out
+  uint32_t *k0 = buf, *k1 = buf + n, *i0 = buf + 2 * n, *i1 = buf + 3 * n;
+  flat_seedkey_kernel<R><<<(unsigned)std::min<size_t>((n + 255) / 256, (size_t)ctx.sm_count * 16), 256, 0, s>>>(
+      L.g, L.seed, L.first_id, L.count, k0, i0);
+  count_launch();
+  int end_bit = 1;
+  while (end_bit < 32 && (1ull << end_bit) < n_vertices) ++end_bit;
+  const int begin_bit = std::max(0, end_bit - AGPM_FLAT_SORT_BITS);
+  size_t temp = 0;
+  AGPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k0, k1, i0, i1, n, begin_bit, end_bit, s));
+  void* tmp = ctx.get(13, temp);
+  AGPM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, k0, k1, i0, i1, n, begin_bit, end_bit, s));
+  count_launch(3);
+  return i1;
+}
+
 template <int K, class R>
 void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
   DeviceCtx& ctx = ctx_for_current_device();
@@ -433,11 +493,14 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
   A.count = L.count;
   A.values = L.values;
   A.bindings = L.bindings;
+  int multi_steps = 0;
   for (int st = 0; st < K - 2; ++st) {
     const unsigned in_m = L.p.in_mask[st], out_m = L.p.out_mask[st];
     A.step_multi[st] = !(__builtin_popcount(in_m) == 1 && out_m == 0);
     A.step_reuse[st] = 0;
+    multi_steps += A.step_multi[st];
   }
+  A.order = flat_order<R>(L, L.g.n, multi_steps, s);
   // Resident 128-thread blocks per SM (the register cap): the kernel hides latency with
   // warps, but shared memory and local-memory stack compete with L1 for the same 256 KB,
   // so 8 blocks (64 registers, no spills, 19 KB of tables each) beat 9 and 10.

@@ -279,6 +279,38 @@ def test_twin_arc_hints_same_samples(agpm, oracle, graphs, strat, pattern):
             np.testing.assert_array_equal(b, ob)
 
 
+@pytest.mark.parametrize("pattern", ["4clique", "5clique", "custom:5:0-1,0-2,1-2,2-3,2-4,3-4"])
+@pytest.mark.parametrize("rng", ["counter", "philox"])
+def test_flat_sorted_order_same_records(agpm, oracle, pattern, rng):
+    """Launches of >= 2^20 ids of a plan with two or more multi-list steps run the flat
+    sampler in seed-sorted processing order (ns_flat.cu: flat_order); values, hits
+    and bindings are written by id, so the records equal the oracle's, and the same
+    ids drawn in smaller (id-ordered) launches."""
+    g = agpm.rmat(14, 16, seed=5).relabel_by_degree()
+    off, nbr = g.arrays()
+    plan = agpm.compile_plan(pattern)
+    dg = agpm.DeviceGraph(g)
+    first, count = (1 << 33) + 12345, (1 << 20) + 77
+    agpm.set_strategy("flat")
+    agpm.set_rng(rng)
+    try:
+        v, h, b = agpm.draw_samples(dg, plan, 9, first, count)[:3]
+        parts = [agpm.draw_samples(dg, plan, 9, first + o, min(1 << 18, count - o))[:3]
+                 for o in range(0, count, 1 << 18)]
+    finally:
+        agpm.set_strategy("auto")
+        agpm.set_rng("counter")
+    np.testing.assert_array_equal(v.view(np.uint64), np.concatenate([p[0] for p in parts]).view(np.uint64))
+    np.testing.assert_array_equal(h, np.concatenate([p[1] for p in parts]))
+    np.testing.assert_array_equal(b, np.concatenate([p[2] for p in parts]))
+    assert int(h.sum()) > 0
+    if rng == "counter":  # the reference stream: the oracle's records
+        ov, oh, ob = oracle.draw_records_mt(off, nbr, g.edge_count, plan, 9, first, count)
+        np.testing.assert_array_equal(v.view(np.uint64), ov.view(np.uint64))
+        np.testing.assert_array_equal(h, oh)
+        np.testing.assert_array_equal(b, ob)
+
+
 def test_prepare_builds_indexes_same_samples(agpm, oracle, graphs):
     """agpm_graph_prepare builds the dense core and twin arcs eagerly: the view
     grows by the twin index at once and draws the oracle's records from its
