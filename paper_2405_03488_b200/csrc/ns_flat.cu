@@ -437,43 +437,57 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
 // 4-clique 5.91 -> 5.72 ms, 5-clique 9.64 -> 8.26; not the triangle (3.16 -> 3.45)
 // or the 4-cycle (5.01 -> 5.05), nor RMAT-22 / 24 with their 8 GB cores (4-clique
 // 8.55 -> 8.86, 4-cycle 7.06 -> 7.74). Sorting by the larger endpoint: 5.70 / 8.84;
-// 12 or 8 key bits instead of 16: 5.99 / 8.61, 5.87 / 8.56. Values and bindings are
-// written by id, so results do not depend on the order.
+// 12 or 8 key bits instead of 16: 5.99 / 8.61, 5.87 / 8.56; the composite key (top 16
+// bits of the smaller endpoint, then top 16 of the larger: samples of neighbouring seed
+// edges intersect the same two lists), four sort passes: 5.57 / 8.24 — the default.
+// Values and bindings are written by id, so results do not depend on the order.
 #ifndef AGPM_FLAT_SORT_KEY
-#define AGPM_FLAT_SORT_KEY 0  // -1 off, 0 smaller seed endpoint, 1 larger seed endpoint
+#define AGPM_FLAT_SORT_KEY 2  // -1 off, 0 smaller seed endpoint, 1 larger seed endpoint, 2 composite (smaller, larger)
 #endif
 #ifndef AGPM_FLAT_SORT_BITS
 #define AGPM_FLAT_SORT_BITS 16
 #endif
+#ifndef AGPM_FLAT_SORT_LOW
+#define AGPM_FLAT_SORT_LOW 16
+#endif
 template <class R>
 __global__ void flat_seedkey_kernel(GraphArgs g, unsigned long long seed, unsigned long long first_id,
-                                    unsigned long long count, uint32_t* __restrict__ keys,
+                                    unsigned long long count, int shift, uint32_t* __restrict__ keys,
                                     uint32_t* __restrict__ idx) {
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < count;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     R rng(seed, 0, first_id + i);
     const unsigned long long arc = __ldg(g.seed_arcs + rng.next_below(g.arcs));
     const uint32_t u = (uint32_t)(arc >> 32), v = (uint32_t)arc;
+#if AGPM_FLAT_SORT_KEY == 2  // composite: top 16 bits of the smaller endpoint, then AGPM_FLAT_SORT_LOW of the larger
+    keys[i] = ((min(u, v) >> shift) << AGPM_FLAT_SORT_LOW) | ((max(u, v) >> shift) >> (16 - AGPM_FLAT_SORT_LOW));
+#else
     keys[i] = AGPM_FLAT_SORT_KEY == 0 ? min(u, v) : max(u, v);
+#endif
     idx[i] = (uint32_t)i;
   }
 }
 
 template <class R>
 const uint32_t* flat_order(const SampleLaunch& L, uint32_t n_vertices, int multi_steps, cudaStream_t s) {
-  if (AGPM_FLAT_SORT_KEY < 0 || multi_steps < 2 || n_vertices > (1u << 21) || L.count < (1ull << 20) ||
-      L.count > 0xffffffffull)
-    return nullptr;
+#ifndef AGPM_FLAT_SORT_ALL
+  if (multi_steps < 2 || n_vertices > (1u << 21)) return nullptr;
+#endif
+  if (AGPM_FLAT_SORT_KEY < 0 || L.count < (1ull << 20) || L.count > 0xffffffffull) return nullptr;
   DeviceCtx& ctx = ctx_for_current_device();
   const size_t n = (size_t)L.count;
   auto* buf = static_cast<uint32_t*>(ctx.get(12, 16 * n));  // keys in/out, idx in/out
   uint32_t *k0 = buf, *k1 = buf + n, *i0 = buf + 2 * n, *i1 = buf + 3 * n;
-  flat_seedkey_kernel<R><<<(unsigned)std::min<size_t>((n + 255) / 256, (size_t)ctx.sm_count * 16), 256, 0, s>>>(
-      L.g, L.seed, L.first_id, L.count, k0, i0);
-  count_launch();
   int end_bit = 1;
   while (end_bit < 32 && (1ull << end_bit) < n_vertices) ++end_bit;
-  const int begin_bit = std::max(0, end_bit - AGPM_FLAT_SORT_BITS);
+  int begin_bit = std::max(0, end_bit - AGPM_FLAT_SORT_BITS);
+  flat_seedkey_kernel<R><<<(unsigned)std::min<size_t>((n + 255) / 256, (size_t)ctx.sm_count * 16), 256, 0, s>>>(
+      L.g, L.seed, L.first_id, L.count, begin_bit, k0, i0);
+  count_launch();
+#if AGPM_FLAT_SORT_KEY == 2
+  end_bit = end_bit - begin_bit + AGPM_FLAT_SORT_LOW;
+  begin_bit = 0;
+#endif
   size_t temp = 0;
   AGPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k0, k1, i0, i1, n, begin_bit, end_bit, s));
   void* tmp = ctx.get(13, temp);
