@@ -425,74 +425,77 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
   }
 }
 
-// Processing order. Sample ids are independent streams, so the order in which a
-// launch works through them is free. Sorted by a seed vertex, consecutive samples
-// (the 32 lanes of a warp, the warps of a block) share that hub: its vertex
-// record, its adjacency list and its dense-core row are then read through L1 / L2
-// instead of DRAM. One pre-pass draws every id's seed arc (the same draw the
-// sampler repeats), a partial radix sort on the key's top bits orders the ids
-// (≈ 0.3 ms per 2^24 ids). Taken where it pays: plans with at least two
-// multi-list steps on graphs whose 64 K dense core stays L2-resident (n <= 2^21)
-// — per 2^24 samples on RMAT-20, id order vs sorted by the smaller seed endpoint:
-// 4-clique 5.91 -> 5.72 ms, 5-clique 9.64 -> 8.26; not the triangle (3.16 -> 3.45)
-// or the 4-cycle (5.01 -> 5.05), nor RMAT-22 / 24 with their 8 GB cores (4-clique
-// 8.55 -> 8.86, 4-cycle 7.06 -> 7.74). Sorting by the larger endpoint: 5.70 / 8.84;
-// 12 or 8 key bits instead of 16: 5.99 / 8.61, 5.87 / 8.56; the composite key (top 16
-// bits of the smaller endpoint, then top 16 of the larger: samples of neighbouring seed
-// edges intersect the same two lists), four sort passes: 5.57 / 8.24 — the default.
-// Values and bindings are written by id, so results do not depend on the order.
-#ifndef AGPM_FLAT_SORT_KEY
-#define AGPM_FLAT_SORT_KEY 2  // -1 off, 0 smaller seed endpoint, 1 larger seed endpoint, 2 composite (smaller, larger)
-#endif
-#ifndef AGPM_FLAT_SORT_BITS
-#define AGPM_FLAT_SORT_BITS 16
-#endif
-#ifndef AGPM_FLAT_SORT_LOW
-#define AGPM_FLAT_SORT_LOW 16
+// Processing order. Sample ids are independent streams and values / bindings are
+// written by id, so the order in which a launch works through its ids is free.
+// In seed-sorted order consecutive samples (the 32 lanes of a warp, the warps of
+// a block) share their hub and mostly their seed edge's neighbourhood: vertex
+// records, adjacency lists and dense-core rows are then read through L1 / L2
+// instead of DRAM. A pre-pass draws every id's seed (the draw the sampler
+// repeats) and a radix sort of (key, id) pairs orders the ids, ~0.3 ms per 2^24.
+// Two keys:
+//   * the seed arc's index (arc order = source vertex, then target): no gather in
+//     the pre-pass and coalesced seed-arc gathers in the sampler — plans with two
+//     multi-list steps (4-clique);
+//   * composite: the top 16 bits of the smaller seed endpoint, then the top 16 of the
+//     larger (neighbouring seed EDGES whichever arc was drawn) — deeper plans.
+// Taken where it pays: >= 2^20 ids, plans with at least two multi-list steps, graphs
+// whose 64 K dense core stays L2-resident (n <= 2^21). Per 2^24 samples on RMAT-20, sort
+// included, id order / arc key / composite key: 4-clique 5.91 / 5.31 / 5.57 ms, 5-clique
+// 9.64 / 8.40 / 8.21, 6-clique 15.7 / 13.9 / 13.3 (smaller endpoint alone 5.70 / 8.26,
+// larger alone 5.70 / 8.84, 12 or 8 key bits 5.99 / 8.61 and 5.87 / 8.56). Not taken
+// where it loses: triangle 3.16 -> 3.45, 4-cycle 5.01 -> 5.05, RMAT-22 / 24 with their
+// 8 GB cores (4-clique 8.55 -> 8.86, 4-cycle 7.06 -> 7.74).
+#ifndef AGPM_FLAT_SORT
+#define AGPM_FLAT_SORT 1  // 0: always id order
 #endif
 template <class R>
 __global__ void flat_seedkey_kernel(GraphArgs g, unsigned long long seed, unsigned long long first_id,
-                                    unsigned long long count, int shift, uint32_t* __restrict__ keys,
-                                    uint32_t* __restrict__ idx) {
+                                    unsigned long long count, bool arc_key, int shift,
+                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ idx) {
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < count;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     R rng(seed, 0, first_id + i);
-    const unsigned long long arc = __ldg(g.seed_arcs + rng.next_below(g.arcs));
-    const uint32_t u = (uint32_t)(arc >> 32), v = (uint32_t)arc;
-#if AGPM_FLAT_SORT_KEY == 2  // composite: top 16 bits of the smaller endpoint, then AGPM_FLAT_SORT_LOW of the larger
-    keys[i] = ((min(u, v) >> shift) << AGPM_FLAT_SORT_LOW) | ((max(u, v) >> shift) >> (16 - AGPM_FLAT_SORT_LOW));
-#else
-    keys[i] = AGPM_FLAT_SORT_KEY == 0 ? min(u, v) : max(u, v);
-#endif
+    const unsigned long long r0 = rng.next_below(g.arcs);  // ns_engine.cpp:29-33
+    uint32_t key;
+    if (arc_key) {
+      key = (uint32_t)(r0 >> shift);
+    } else {
+      const unsigned long long arc = __ldg(g.seed_arcs + r0);
+      const uint32_t u = (uint32_t)(arc >> 32), v = (uint32_t)arc;
+      key = ((min(u, v) >> shift) << 16) | (max(u, v) >> shift);
+    }
+    keys[i] = key;
     idx[i] = (uint32_t)i;
   }
 }
 
 template <class R>
-const uint32_t* flat_order(const SampleLaunch& L, uint32_t n_vertices, int multi_steps, cudaStream_t s) {
-#ifndef AGPM_FLAT_SORT_ALL
-  if (multi_steps < 2 || n_vertices > (1u << 21)) return nullptr;
-#endif
-  if (AGPM_FLAT_SORT_KEY < 0 || L.count < (1ull << 20) || L.count > 0xffffffffull) return nullptr;
+const uint32_t* flat_order(const SampleLaunch& L, int multi_steps, cudaStream_t s) {
+  if (!AGPM_FLAT_SORT || multi_steps < 2 || L.g.n > (1u << 21) || L.count < (1ull << 20) ||
+      L.count > 0xffffffffull)
+    return nullptr;
   DeviceCtx& ctx = ctx_for_current_device();
   const size_t n = (size_t)L.count;
-  auto* buf = static_cast<uint32_t*>(ctx.get(12, 16 * n));  // keys in/out, idx in/out
+  auto* buf = static_cast<uint32_t*>(ctx.get(12, 16 * n));  // keys in/out, ids in/out
   uint32_t *k0 = buf, *k1 = buf + n, *i0 = buf + 2 * n, *i1 = buf + 3 * n;
-  int end_bit = 1;
-  while (end_bit < 32 && (1ull << end_bit) < n_vertices) ++end_bit;
-  int begin_bit = std::max(0, end_bit - AGPM_FLAT_SORT_BITS);
+  auto bits_of = [](unsigned long long x) {
+    int b = 1;
+    while (b < 63 && (1ull << b) < x) ++b;
+    return b;
+  };
+  const bool arc_key = multi_steps == 2;
+  // keys are 32 bits: the top 32 bits of the arc index, or 16 + 16 top bits of the endpoints
+  const int width = arc_key ? bits_of(L.g.arcs) : bits_of(L.g.n);
+  const int shift = std::max(0, width - (arc_key ? 32 : 16));
+  const int end_bit = arc_key ? width - shift : 2 * 16;
   flat_seedkey_kernel<R><<<(unsigned)std::min<size_t>((n + 255) / 256, (size_t)ctx.sm_count * 16), 256, 0, s>>>(
-      L.g, L.seed, L.first_id, L.count, begin_bit, k0, i0);
+      L.g, L.seed, L.first_id, L.count, arc_key, shift, k0, i0);
   count_launch();
-#if AGPM_FLAT_SORT_KEY == 2
-  end_bit = end_bit - begin_bit + AGPM_FLAT_SORT_LOW;
-  begin_bit = 0;
-#endif
   size_t temp = 0;
-  AGPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k0, k1, i0, i1, n, begin_bit, end_bit, s));
+  AGPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k0, k1, i0, i1, n, 0, end_bit, s));
   void* tmp = ctx.get(13, temp);
-  AGPM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, k0, k1, i0, i1, n, begin_bit, end_bit, s));
-  count_launch(3);
+  AGPM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, k0, k1, i0, i1, n, 0, end_bit, s));
+  count_launch(1 + (end_bit + 7) / 8);  // histogram + one onesweep pass per 8 key bits
   return i1;
 }
 
@@ -514,7 +517,7 @@ void run_flat_k(const SampleLaunch& L, cudaStream_t s) {
     A.step_reuse[st] = 0;
     multi_steps += A.step_multi[st];
   }
-  A.order = flat_order<R>(L, L.g.n, multi_steps, s);
+  A.order = flat_order<R>(L, multi_steps, s);
   // Resident 128-thread blocks per SM (the register cap): the kernel hides latency with
   // warps, but shared memory and local-memory stack compete with L1 for the same 256 KB,
   // so 8 blocks (64 registers, no spills, 19 KB of tables each) beat 9 and 10.
