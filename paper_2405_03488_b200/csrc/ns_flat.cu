@@ -10,6 +10,9 @@
 #define AGPM_FLAT_DESC_ALIGN 16
 #endif
 #define AGPM_DESC_ALIGN AGPM_FLAT_DESC_ALIGN
+#ifndef AGPM_FLAT_DEDUP
+#define AGPM_FLAT_DEDUP 1  // same-seed samples share the first multi-list step (see fr_flat_kernel)
+#endif
 #ifndef AGPM_FLAT_HINT_LOCAL_K
 #define AGPM_FLAT_HINT_LOCAL_K 4
 #endif
@@ -230,6 +233,28 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       const bool wps = dsz > (uint32_t)kFlatW * 32 - 16;  // padded to whole octets, a fast driver still fits a round
       unsigned long long cnt = 0;
       uint32_t o_pick = 0;
+#if AGPM_FLAT_DEDUP
+      // Samples with the same seed pair share S_2 (the first multi-list step of a plan
+      // that starts with one depends on the seed alone). In seed-sorted order they are
+      // neighbours (2^24 draws over 3.1e7 arcs: 22 % of the samples repeat an arc of the
+      // launch): one lane enumerates the driver, the others count and pick from its
+      // ballot segment with their own streams. The key is the seed pair and which of
+      // its two lists drives: equal exact ranges may resolve the driver either way
+      // depending on the hints the drawn arc direction gave (ids < 2^31: the sorted
+      // order is only taken up to 2^21 vertices).
+      const bool dedup = j == 2 && A.order != nullptr;
+      int leader = lane;
+      if (dedup) {
+        const unsigned long long key =
+            pend >= 0 && !wps ? ((unsigned long long)(my.owner[0] | (my.drv_pos << 31)) << 32) | my.owner[1]
+                              : ~(unsigned long long)lane;
+        leader = __ffs(__match_any_sync(FULL, key)) - 1;
+      }
+      const bool follower = leader != lane;
+#else
+      constexpr bool dedup = false, follower = false;
+      constexpr int leader = 0;
+#endif
       // long drivers: the whole warp on one sample, counted, then replayed up to
       // the r-th live element
       for (unsigned bm = __ballot_sync(FULL, wps); bm; bm &= bm - 1) {
@@ -273,7 +298,7 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       // fast samples first, then the others (each class flattened on its own)
       for (int cls = 0; cls < 2; ++cls) {
       const bool allfast = cls == 0;
-      const bool part = pend >= 0 && !wps && fast == allfast;
+      const bool part = pend >= 0 && !wps && fast == allfast && !follower;
       // fast class: units are octets of the 32-B-aligned cover of the driver range
       const uint32_t head = (uint32_t)(reinterpret_cast<unsigned long long>(my.drv) >> 2) & 7u;
       const uint32_t sz = !part ? 0u : allfast ? (head + dsz + 7) >> 3 : dsz;
@@ -356,7 +381,17 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
           if (lane == 0) bal[it] = b;
         }
         __syncwarp();
-        if (inr) {
+        bool mine = inr;
+        if (dedup) {  // a follower reads its leader's segment
+          const bool l_inr = __shfl_sync(FULL, inr, leader);
+          const uint32_t lb0 = __shfl_sync(FULL, b0, leader), lb1 = __shfl_sync(FULL, b1, leader);
+          if (follower && l_inr && fast == allfast) {
+            mine = true;
+            b0 = lb0;
+            b1 = lb1;
+          }
+        }
+        if (mine) {
           const uint32_t w0 = b0 >> 5, w1 = (b1 - 1) >> 5;
           unsigned long long c = 0;
           for (uint32_t w = w0; w <= w1; ++w) c += __popc(bal[w] & seg_mask(w, b0, b1));
