@@ -457,7 +457,15 @@ def run_gpu(args):
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src,
                          "bmin_bytes_per_sample": bmin_per_sample, "kernel_ms": kern_ms,
-                         "kernel_share_of_step": kern_ms / ms_per_step},
+                         "kernel_share_of_step": kern_ms / ms_per_step,
+                         "dram_frac_profiled": (traffic / (kern_ms / 1000.0) / 1e9 / peak) if traffic else None,
+                         "note": "achieved = E[B_min] (SURVEY 8(d) per-sample sector model, counted on the device) "
+                                 "x samples per launch / sampling-launch time (seed-key pre-pass, radix sort and "
+                                 "fr_flat_kernel together). B_min models every sample on its own; the launch works "
+                                 "in seed-sorted order and samples with the same seed pair share their first "
+                                 "intersection, so it moves fewer DRAM bytes than B_min (traffic) and frac can "
+                                 "exceed 1; dram_frac_profiled = the profiled DRAM bytes / this run's launch time "
+                                 "/ peak"},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

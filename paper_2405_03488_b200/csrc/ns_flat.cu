@@ -473,13 +473,22 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
 //     multi-list steps (4-clique);
 //   * composite: the top 16 bits of the smaller seed endpoint, then the top 16 of the
 //     larger (neighbouring seed EDGES whichever arc was drawn) — deeper plans.
-// Taken where it pays: >= 2^20 ids, plans with at least two multi-list steps, graphs
-// whose 64 K dense core stays L2-resident (n <= 2^21). Per 2^24 samples on RMAT-20, sort
-// included, id order / arc key / composite key: 4-clique 5.91 / 5.31 / 5.57 ms, 5-clique
-// 9.64 / 8.40 / 8.21, 6-clique 15.7 / 13.9 / 13.3 (smaller endpoint alone 5.70 / 8.26,
-// larger alone 5.70 / 8.84, 12 or 8 key bits 5.99 / 8.61 and 5.87 / 8.56). Not taken
-// where it loses: triangle 3.16 -> 3.45, 4-cycle 5.01 -> 5.05, RMAT-22 / 24 with their
-// 8 GB cores (4-clique 8.55 -> 8.86, 4-cycle 7.06 -> 7.74).
+// Taken where it pays: launches of >= 2^20 ids of plans with at least two multi-list
+// steps; the arc key up to 2^25 vertices, the composite key up to 2^22. Per 2^24 samples,
+// sort included, id order -> sorted (with the shared first step, see the kernel):
+//   arc key, 4-clique: RMAT-20 5.91 -> 5.03 ms, RMAT-21 7.15 -> 6.30, RMAT-22 8.55 -> 7.66,
+//     RMAT-23 10.24 -> 9.53, RMAT-24 12.76 -> 11.96, RMAT-25 16.17 -> 15.43 (the top 24 key
+//     bits: three sort passes; all 25 bits, four passes: RMAT-20 5.15; 16 bits: 5.38);
+//   composite key: RMAT-20 5-clique 9.64 -> 7.97, 6-clique 15.7 -> 12.9, RMAT-22 5-clique
+//     12.0 -> 11.7; beyond it loses (RMAT-23 5-clique 14.57 -> 14.67, RMAT-24 16.9 -> 17.8);
+//     on the RMAT-20 4-clique: 5.57 (arc key 5.31, before the shared step); the smaller
+//     endpoint alone 5.70 / 5-clique 8.26, the larger alone 5.70 / 8.84, 12 or 8 bits
+//     5.99 / 8.61 and 5.87 / 8.56.
+// Not taken where it loses: plans with one multi-list step (triangle 3.16 -> 3.45, 4-cycle
+// 5.01 -> 5.05; RMAT-22 4-cycle 7.06 -> 7.74).
+#ifndef AGPM_FLAT_ARC_BITS
+#define AGPM_FLAT_ARC_BITS 24
+#endif
 #ifndef AGPM_FLAT_SORT
 #define AGPM_FLAT_SORT 1  // 0: always id order
 #endif
@@ -506,8 +515,11 @@ __global__ void flat_seedkey_kernel(GraphArgs g, unsigned long long seed, unsign
 
 template <class R>
 const uint32_t* flat_order(const SampleLaunch& L, int multi_steps, cudaStream_t s) {
-  if (!AGPM_FLAT_SORT || multi_steps < 2 || L.g.n > (1u << 21) || L.count < (1ull << 20) ||
-      L.count > 0xffffffffull)
+  // (16 B of sort scratch per id: launches beyond 2^26 ids — the library's own drivers
+  // launch at most 2^24 at a time — keep id order)
+  const bool arc_key = multi_steps == 2;
+  if (!AGPM_FLAT_SORT || multi_steps < 2 || L.g.n > (arc_key ? 1u << 25 : 1u << 22) || L.count < (1ull << 20) ||
+      L.count > (1ull << 26))
     return nullptr;
   DeviceCtx& ctx = ctx_for_current_device();
   const size_t n = (size_t)L.count;
@@ -518,10 +530,10 @@ const uint32_t* flat_order(const SampleLaunch& L, int multi_steps, cudaStream_t 
     while (b < 63 && (1ull << b) < x) ++b;
     return b;
   };
-  const bool arc_key = multi_steps == 2;
-  // keys are 32 bits: the top 32 bits of the arc index, or 16 + 16 top bits of the endpoints
+  // keys: the top AGPM_FLAT_ARC_BITS bits of the arc index (three 8-bit sort passes), or
+  // 16 + 16 top bits of the endpoints (four)
   const int width = arc_key ? bits_of(L.g.arcs) : bits_of(L.g.n);
-  const int shift = std::max(0, width - (arc_key ? 32 : 16));
+  const int shift = std::max(0, width - (arc_key ? AGPM_FLAT_ARC_BITS : 16));
   const int end_bit = arc_key ? width - shift : 2 * 16;
   flat_seedkey_kernel<R><<<(unsigned)std::min<size_t>((n + 255) / 256, (size_t)ctx.sm_count * 16), 256, 0, s>>>(
       L.g, L.seed, L.first_id, L.count, arc_key, shift, k0, i0);

@@ -100,6 +100,17 @@ def test_config3_records_with_twin_hints(agpm, oracle, rmat22, spec, strategy):
         agpm.set_strategy("auto")
 
 
+@pytest.mark.parametrize("spec", ["4clique", "5clique"])
+def test_config3_sorted_launch(agpm, oracle, rmat22, spec):
+    """A launch of 2^20 ids: the flat sampler works through it in seed-sorted order (arc
+    key for the 4-clique, composite key for the 5-clique) with shared first steps
+    (ns_flat.cu: flat_order) — same records as the oracle at scale."""
+    dg, host, info = rmat22
+    plan = agpm.compile_plan(spec)
+    assert agpm.strategy_for(dg, plan, 1 << 20) == "flat"
+    assert _records_equal(agpm, oracle, dg, host, info["edge_count"], plan, OFFSETS[1] + 7, 1 << 20) > 0
+
+
 def test_config3_online(agpm, oracle, rmat22):
     dg, host, info = rmat22
     r = _online_equal(agpm, oracle, dg, host, info["edge_count"], agpm.compile_plan("4cycle"))
@@ -122,6 +133,12 @@ def test_config5_class_records(agpm, oracle, rmat25, spec, strategy):
     finally:
         agpm.set_strategy("auto")
     assert sum(hits) > 0
+
+
+def test_config5_class_sorted_launch(agpm, oracle, rmat25):
+    """RMAT-25, 4-clique, one 2^20-id launch: seed-sorted order on the arc key (taken up to 2^25 vertices)."""
+    dg, host, info = rmat25
+    _records_equal(agpm, oracle, dg, host, info["edge_count"], agpm.compile_plan("4clique"), OFFSETS[0] + 3, 1 << 20)
 
 
 def test_config5_class_online(agpm, oracle, rmat25):
