@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 profiling recipe (GPU box, repo root). Every ncu run follows a clean
 # run of the same command; numbers printed under ncu are never bench values.
-OUT=${OUT:-gpurun_out/prof5}
+OUT=${OUT:-gpurun_out/prof6}
 mkdir -p $OUT
 python bench.py --steps 10 --warmup 3 > $OUT/bench.log 2>&1 || exit 1
 tail -1 $OUT/bench.log > $OUT/bench_line.json
@@ -12,7 +12,7 @@ M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_secto
 # 2. per-kernel traffic (auto strategy, auto core): flat 4-clique RMAT-20 (config 2), flat 4-cycle RMAT-22
 #    (config 3), frontier 4-clique RMAT-27 (config 5), the 4-cycle pair count (config 3 region split)
 python tools/prof_ns.py auto 4clique 2 -1 rmat20 > $OUT/clean_flat.log 2>&1 && \
-ncu --metrics $M --clock-control none --csv --log-file $OUT/traffic_flat_rmat20.csv -k 'regex:fr_|flat_seedkey' python tools/prof_ns.py auto 4clique 2 -1 rmat20 > /dev/null 2>&1
+ncu --metrics $M --clock-control none --csv --log-file $OUT/traffic_flat_rmat20.csv -k 'regex:fr_|flat_seedkey|RadixSort' python tools/prof_ns.py auto 4clique 2 -1 rmat20 > /dev/null 2>&1
 python tools/prof_ns.py auto 4cycle 2 -1 rmat22 > $OUT/clean_c3.log 2>&1 && \
 ncu --metrics $M --clock-control none --csv --log-file $OUT/traffic_4cycle_rmat22.csv -k regex:fr_ python tools/prof_ns.py auto 4cycle 2 -1 rmat22 > /dev/null 2>&1
 python tools/prof_ns.py auto 4clique 2 -1 rmat27 > $OUT/clean_c5.log 2>&1 && \
