@@ -21,11 +21,11 @@ python tools/prof_c4.py 22 2 > $OUT/clean_c4.log 2>&1 && \
 ncu --metrics $M --clock-control none --csv --log-file $OUT/traffic_c4_rmat22.csv -k regex:c4_ python tools/prof_c4.py 22 1 > /dev/null 2>&1
 # 3. full captures (with source): the flat kernel's 2nd launch on config 2 and on config 3, the
 #    frontier isect on RMAT-27 4-clique (its 3rd launch = step 1 of the second pass)
-ncu --set full --import-source on --clock-control none -k regex:fr_flat -s 1 -c 1 -o /tmp/flat_full \
+ncu --set full --import-source on --clock-control none -k regex:fr_flat -s 1 -c 1 -f -o /tmp/flat_full \
     python tools/prof_ns.py auto 4clique 2 -1 rmat20 > $OUT/ncu_full_flat.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:fr_flat -s 1 -c 1 -o /tmp/flat_c3_full \
+ncu --set full --import-source on --clock-control none -k regex:fr_flat -s 1 -c 1 -f -o /tmp/flat_c3_full \
     python tools/prof_ns.py auto 4cycle 2 -1 rmat22 > $OUT/ncu_full_flat_c3.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:fr_isect -s 2 -c 1 -o /tmp/isect_full \
+ncu --set full --import-source on --clock-control none -k regex:fr_isect -s 2 -c 1 -f -o /tmp/isect_full \
     python tools/prof_ns.py auto 4clique 2 -1 rmat27 > $OUT/ncu_full_isect.log 2>&1
 for r in flat_full flat_c3_full isect_full; do
   ncu -i /tmp/$r.ncu-rep --page raw --csv > $OUT/${r}_raw.csv 2>/dev/null
