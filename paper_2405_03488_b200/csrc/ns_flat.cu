@@ -470,17 +470,20 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
 // Two keys:
 //   * the seed arc's index (arc order = source vertex, then target): no gather in
 //     the pre-pass and coalesced seed-arc gathers in the sampler — plans with two
-//     multi-list steps (4-clique);
+//     multi-list steps (4-clique), and every plan above 2^22 vertices;
 //   * composite: the top 16 bits of the smaller seed endpoint, then the top 16 of the
-//     larger (neighbouring seed EDGES whichever arc was drawn) — deeper plans.
+//     larger (neighbouring seed EDGES whichever arc was drawn) — deeper plans up to
+//     2^22 vertices.
 // Taken where it pays: launches of >= 2^20 ids of plans with at least two multi-list
-// steps; the arc key up to 2^25 vertices, the composite key up to 2^22. Per 2^24 samples,
+// steps on graphs up to 2^25 vertices. Per 2^24 samples,
 // sort included, id order -> sorted (with the shared first step, see the kernel):
 //   arc key, 4-clique: RMAT-20 5.91 -> 5.03 ms, RMAT-21 7.15 -> 6.30, RMAT-22 8.55 -> 7.66,
 //     RMAT-23 10.24 -> 9.53, RMAT-24 12.76 -> 11.96, RMAT-25 16.17 -> 15.43 (the top 24 key
 //     bits: three sort passes; all 25 bits, four passes: RMAT-20 5.15; 16 bits: 5.38);
 //   composite key: RMAT-20 5-clique 9.64 -> 7.97, 6-clique 15.7 -> 12.9, RMAT-22 5-clique
-//     12.0 -> 11.7; beyond it loses (RMAT-23 5-clique 14.57 -> 14.67, RMAT-24 16.9 -> 17.8);
+//     12.0 -> 11.7; beyond it loses (RMAT-23 5-clique 14.57 -> 14.67, RMAT-24 16.9 -> 17.8)
+//     where the arc key still wins (5-clique RMAT-23 14.53 -> 13.53, RMAT-24 17.06 -> 16.04,
+//     RMAT-25 21.19 -> 20.12; 6-clique RMAT-24 24.3 -> 22.6);
 //     on the RMAT-20 4-clique: 5.57 (arc key 5.31, before the shared step); the smaller
 //     endpoint alone 5.70 / 5-clique 8.26, the larger alone 5.70 / 8.84, 12 or 8 bits
 //     5.99 / 8.61 and 5.87 / 8.56.
@@ -517,8 +520,8 @@ template <class R>
 const uint32_t* flat_order(const SampleLaunch& L, int multi_steps, cudaStream_t s) {
   // (16 B of sort scratch per id: launches beyond 2^26 ids — the library's own drivers
   // launch at most 2^24 at a time — keep id order)
-  const bool arc_key = multi_steps == 2;
-  if (!AGPM_FLAT_SORT || multi_steps < 2 || L.g.n > (arc_key ? 1u << 25 : 1u << 22) || L.count < (1ull << 20) ||
+  const bool arc_key = multi_steps == 2 || L.g.n > (1u << 22);
+  if (!AGPM_FLAT_SORT || multi_steps < 2 || L.g.n > (1u << 25) || L.count < (1ull << 20) ||
       L.count > (1ull << 26))
     return nullptr;
   DeviceCtx& ctx = ctx_for_current_device();

@@ -135,10 +135,11 @@ def test_config5_class_records(agpm, oracle, rmat25, spec, strategy):
     assert sum(hits) > 0
 
 
-def test_config5_class_sorted_launch(agpm, oracle, rmat25):
-    """RMAT-25, 4-clique, one 2^20-id launch: seed-sorted order on the arc key (taken up to 2^25 vertices)."""
+@pytest.mark.parametrize("spec", ["4clique", "5clique"])
+def test_config5_class_sorted_launch(agpm, oracle, rmat25, spec):
+    """RMAT-25, one 2^20-id launch: seed-sorted order on the arc key (every plan above 2^22 vertices)."""
     dg, host, info = rmat25
-    _records_equal(agpm, oracle, dg, host, info["edge_count"], agpm.compile_plan("4clique"), OFFSETS[0] + 3, 1 << 20)
+    _records_equal(agpm, oracle, dg, host, info["edge_count"], agpm.compile_plan(spec), OFFSETS[0] + 3, 1 << 20)
 
 
 def test_config5_class_online(agpm, oracle, rmat25):
