@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
 //   * composite: the top 16 bits of the smaller seed endpoint, then the top 16 of the
 //     larger (neighbouring seed EDGES whichever arc was drawn) — deeper plans up to
 //     2^22 vertices.
-// Taken where it pays: launches of >= 2^20 ids of plans with at least two multi-list
-// steps on graphs up to 2^25 vertices. Per 2^24 samples,
+// Taken where it pays: launches of >= 2^20 ids; plans with at least two multi-list
+// steps on graphs up to 2^25 vertices, plans with one up to 2^21. Per 2^24 samples,
 // sort included, id order -> sorted (with the shared first step, see the kernel):
 //   arc key, 4-clique: RMAT-20 5.91 -> 5.03 ms, RMAT-21 7.15 -> 6.30, RMAT-22 8.55 -> 7.66,
 //     RMAT-23 10.24 -> 9.53, RMAT-24 12.76 -> 11.96, RMAT-25 16.17 -> 15.43 (the top 24 key
@@ -487,8 +487,10 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
 //     on the RMAT-20 4-clique: 5.57 (arc key 5.31, before the shared step); the smaller
 //     endpoint alone 5.70 / 5-clique 8.26, the larger alone 5.70 / 8.84, 12 or 8 bits
 //     5.99 / 8.61 and 5.87 / 8.56.
-// Not taken where it loses: plans with one multi-list step (triangle 3.16 -> 3.45, 4-cycle
-// 5.01 -> 5.05; RMAT-22 4-cycle 7.06 -> 7.74).
+//   arc key, one multi-list step: RMAT-20 triangle 3.19 -> 2.92, 4-cycle 5.12 -> 4.67; not
+//     beyond 2^21 vertices (RMAT-22 triangle 5.20 -> 5.20, 4-cycle 7.15 -> 7.30; with the
+//     composite key RMAT-20 triangle 3.16 -> 3.45, RMAT-22 4-cycle 7.06 -> 7.74);
+//   RMAT-26 4-clique (512 K core): 22.4 -> 22.6, not taken.
 #ifndef AGPM_FLAT_ARC_BITS
 #define AGPM_FLAT_ARC_BITS 24
 #endif
@@ -520,8 +522,9 @@ template <class R>
 const uint32_t* flat_order(const SampleLaunch& L, int multi_steps, cudaStream_t s) {
   // (16 B of sort scratch per id: launches beyond 2^26 ids — the library's own drivers
   // launch at most 2^24 at a time — keep id order)
-  const bool arc_key = multi_steps == 2 || L.g.n > (1u << 22);
-  if (!AGPM_FLAT_SORT || multi_steps < 2 || L.g.n > (1u << 25) || L.count < (1ull << 20) ||
+  const bool arc_key = multi_steps <= 2 || L.g.n > (1u << 22);
+  if (!AGPM_FLAT_SORT || multi_steps < 1 || L.g.n > (multi_steps == 1 ? 1u << 21 : 1u << 25) ||
+      L.count < (1ull << 20) ||
       L.count > (1ull << 26))
     return nullptr;
   DeviceCtx& ctx = ctx_for_current_device();

@@ -279,10 +279,10 @@ def test_twin_arc_hints_same_samples(agpm, oracle, graphs, strat, pattern):
             np.testing.assert_array_equal(b, ob)
 
 
-@pytest.mark.parametrize("pattern", ["4clique", "5clique", "custom:5:0-1,0-2,1-2,2-3,2-4,3-4"])
+@pytest.mark.parametrize("pattern", ["triangle", "4cycle", "4clique", "5clique", "custom:5:0-1,0-2,1-2,2-3,2-4,3-4"])
 @pytest.mark.parametrize("rng", ["counter", "philox"])
 def test_flat_sorted_order_same_records(agpm, oracle, pattern, rng):
-    """Launches of >= 2^20 ids of a plan with two or more multi-list steps run the flat
+    """Launches of >= 2^20 ids run the flat
     sampler in seed-sorted processing order (ns_flat.cu: flat_order); values, hits
     and bindings are written by id, so the records equal the oracle's, and the same
     ids drawn in smaller (id-ordered) launches."""
