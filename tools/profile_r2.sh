@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 profiling recipe (GPU box, repo root). Every ncu run follows a clean
 # run of the same command; numbers printed under ncu are never bench values.
-OUT=${OUT:-gpurun_out/prof6}
+OUT=${OUT:-gpurun_out/prof7}
 mkdir -p $OUT
 python bench.py --steps 10 --warmup 3 > $OUT/bench.log 2>&1 || exit 1
 tail -1 $OUT/bench.log > $OUT/bench_line.json
