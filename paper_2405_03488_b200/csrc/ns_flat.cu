@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kFlatThreads, kMinB) fr_flat_kernel(const Fron
       // ballot segment with their own streams. The key is the seed pair and which of
       // its two lists drives: equal exact ranges may resolve the driver either way
       // depending on the hints the drawn arc direction gave (ids < 2^31: the sorted
-      // order is only taken up to 2^21 vertices).
+      // order is only taken up to 2^25 vertices).
       const bool dedup = j == 2 && A.order != nullptr;
       int leader = lane;
       if (dedup) {
